@@ -1,0 +1,313 @@
+// Per-batch and per-dictionary setup kernels:
+//   default_lambda  (prox.py:153-161)      lambda_p = beta * max_k |(A^H b_p)_k|
+//   derive_seeds    (cli.py:102, rng.py:17-29)  per-pixel RBPG seeds from (run_seed, pixel_id)
+//   power iteration (solver.py:167-188)    sigma_max^2 of column ranges, fp64
+#include <float.h>
+
+#include "common.cuh"
+#include "setup.h"
+
+namespace tb {
+
+// ------------------------------------------------------------------ default lambda
+// One warp per pixel (grid-stride over pixels), lanes own columns; b broadcast from shared.
+__global__ void __launch_bounds__(256) default_lambda_kernel(const float2* __restrict__ A, int n, int m,
+                                                             const float2* __restrict__ B, long long P,
+                                                             double beta, float* __restrict__ lam) {
+  extern __shared__ float2 sb[];  // [warps][n]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float2* bw = sb + (size_t)warp * n;
+  for (long long p = (long long)blockIdx.x * nw + warp; p < P; p += (long long)gridDim.x * nw) {
+    for (int i = lane; i < n; i += 32) bw[i] = B[(size_t)p * n + i];
+    __syncwarp();
+    float best = 0.f;
+    for (int c = lane; c < m; c += 32) {
+      float2 acc = make_float2(0.f, 0.f);
+      for (int i = 0; i < n; ++i) cfma_conj(acc, __ldg(&A[(size_t)i * m + c]), bw[i]);
+      best = fmaxf(best, cabsf(acc));
+    }
+    best = warp_maxf(best);
+    if (lane == 0) lam[p] = (float)(beta * (double)best);
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B, long long P, double beta,
+                                  float* lam, int num_sms, cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  const int warps = 8;
+  long long blocks = (P + warps - 1) / warps;
+  if (blocks > (long long)num_sms * 8) blocks = (long long)num_sms * 8;
+  size_t smem = (size_t)warps * n * sizeof(float2);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(default_lambda_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  default_lambda_kernel<<<(int)blocks, warps * 32, smem, st>>>(A, n, m, B, P, beta, lam);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ derive_seed
+// integers(0, 2^63-1) on substream(run_seed, pixel_id): Lemire with range 2^63-1.
+__global__ void derive_seeds_kernel(uint64_t run_seed, long long first, long long P, uint64_t* seeds) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= P) return;
+  Philox4x64 s;
+  philox_init(s, run_seed, (uint64_t)(first + idx));
+  const uint64_t rng_excl = 0x7FFFFFFFFFFFFFFFull;
+  for (;;) {
+    uint64_t raw = philox_next(s);
+    uint64_t lo = raw * rng_excl, hi = __umul64hi(raw, rng_excl);
+    if (lo >= 2ull) {
+      seeds[idx] = hi;
+      return;
+    }
+  }
+}
+
+cudaError_t launch_derive_seeds(uint64_t run_seed, long long first, long long P, uint64_t* seeds, cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  derive_seeds_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(run_seed, first, P, seeds);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ power iteration
+// Single-CTA-per-range variant: the whole iteration loop runs on device.
+// v: complex128 work vectors, one per range, concatenated (initialised with the start vectors).
+struct PowerRange {
+  long long start, stop, voff;
+};
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += red[w];
+  return t;
+}
+
+__global__ void __launch_bounds__(256) power_iter_small_kernel(const float2* __restrict__ A, int n, int m,
+                                                               const PowerRange* ranges, double2* v,
+                                                               double2* uscratch, int max_iter, double rtol,
+                                                               double* out) {
+  extern __shared__ double2 w[];  // [n]
+  __shared__ double red[32];
+  const PowerRange R = ranges[blockIdx.x];
+  const long long width = R.stop - R.start;
+  double2* vv = v + R.voff;
+  double2* uu = uscratch + R.voff;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (width == 1) {  // solver.py:170-171
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      float2 a = A[(size_t)i * m + R.start];
+      s += (double)a.x * a.x + (double)a.y * a.y;
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+    return;
+  }
+  double prev = 0.0, result = 0.0;
+  bool done = false;
+  for (int it = 0; it < max_iter && !done; ++it) {
+    // w = A v
+    for (int i = warp; i < n; i += nw) {
+      double re = 0.0, im = 0.0;
+      for (long long c = lane; c < width; c += 32) {
+        float2 a = A[(size_t)i * m + R.start + c];
+        double2 x = vv[c];
+        re += (double)a.x * x.x - (double)a.y * x.y;
+        im += (double)a.x * x.y + (double)a.y * x.x;
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == 0) w[i] = make_double2(re, im);
+    }
+    __syncthreads();
+    double s2 = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s2 += w[i].x * w[i].x + w[i].y * w[i].y;
+    const double cur = block_sum(s2, red);
+    // u = A^H w, ||u||
+    double nu2 = 0.0;
+    for (long long c = threadIdx.x; c < width; c += blockDim.x) {
+      double re = 0.0, im = 0.0;
+      for (int i = 0; i < n; ++i) {
+        float2 a = A[(size_t)i * m + R.start + c];
+        re += (double)a.x * w[i].x + (double)a.y * w[i].y;
+        im += (double)a.x * w[i].y - (double)a.y * w[i].x;
+      }
+      uu[c] = make_double2(re, im);
+      nu2 += re * re + im * im;
+    }
+    const double nu = sqrt(block_sum(nu2, red));
+    if (nu == 0.0) {
+      result = 0.0;
+      done = true;
+      break;
+    }
+    const double inv = 1.0 / nu;
+    for (long long c = threadIdx.x; c < width; c += blockDim.x) {
+      double2 u = uu[c];
+      vv[c] = make_double2(u.x * inv, u.y * inv);
+    }
+    __syncthreads();
+    if (fabs(cur - prev) <= rtol * fmax(cur, 1e-300)) {
+      result = cur;
+      done = true;
+      break;
+    }
+    prev = cur;
+    result = prev;
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = result;
+}
+
+cudaError_t launch_power_small(const float2* A, int n, int m, const long long* starts, const long long* stops,
+                               int num_ranges, double2* v, double2* uscratch, int max_iter, double rtol,
+                               double* out_dev, cudaStream_t st) {
+  PowerRange* hr = new PowerRange[num_ranges];
+  long long off = 0;
+  for (int r = 0; r < num_ranges; ++r) {
+    hr[r].start = starts[r];
+    hr[r].stop = stops[r];
+    hr[r].voff = off;
+    off += stops[r] - starts[r];
+  }
+  PowerRange* dr = nullptr;
+  cudaError_t e = cudaMallocAsync(&dr, sizeof(PowerRange) * num_ranges, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dr, hr, sizeof(PowerRange) * num_ranges, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  delete[] hr;
+  if (e != cudaSuccess) return e;
+  size_t smem = (size_t)n * sizeof(double2);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(power_iter_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  power_iter_small_kernel<<<num_ranges, 256, smem, st>>>(A, n, m, dr, v, uscratch, max_iter, rtol, out_dev);
+  e = cudaGetLastError();
+  cudaFreeAsync(dr, st);
+  return e;
+}
+
+// Multi-CTA variant for wide ranges (cfg4/cfg5 full dictionaries): host-driven iteration with
+// fixed-order partial reductions (deterministic), one convergence read-back per iteration.
+__global__ void __launch_bounds__(256) pw_forward_partial(const float2* __restrict__ A, int n, int m, long long start,
+                                                          long long width, const double2* __restrict__ v,
+                                                          double inv_scale, int cols_per_cta, double2* partial) {
+  // partial[cta][i] = sum_{c in cta tile} A[i][start+c] * v[c] * inv_scale
+  const long long c0 = (long long)blockIdx.x * cols_per_cta;
+  const long long c1 = min(c0 + (long long)cols_per_cta, width);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < n; i += nw) {
+    double re = 0.0, im = 0.0;
+    for (long long c = c0 + lane; c < c1; c += 32) {
+      float2 a = A[(size_t)i * m + start + c];
+      double2 x = v[c];
+      re += (double)a.x * x.x - (double)a.y * x.y;
+      im += (double)a.x * x.y + (double)a.y * x.x;
+    }
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == 0) partial[(size_t)blockIdx.x * n + i] = make_double2(re * inv_scale, im * inv_scale);
+  }
+}
+
+__global__ void pw_reduce_w(const double2* partial, int nparts, int n, double2* w, double* cur) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int p = 0; p < nparts; ++p) {
+      double2 t = partial[(size_t)p * n + i];
+      re += t.x;
+      im += t.y;
+    }
+    w[i] = make_double2(re, im);
+    s += re * re + im * im;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *cur = s;
+}
+
+__global__ void __launch_bounds__(256) pw_adjoint(const float2* __restrict__ A, int n, int m, long long start,
+                                                  long long width, const double2* __restrict__ w, double2* u,
+                                                  double* nrm_partial) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < width; c += (long long)gridDim.x * blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int i = 0; i < n; ++i) {
+      float2 a = A[(size_t)i * m + start + c];
+      double2 ww = w[i];
+      re += (double)a.x * ww.x + (double)a.y * ww.y;
+      im += (double)a.x * ww.y - (double)a.y * ww.x;
+    }
+    u[c] = make_double2(re, im);
+    s += re * re + im * im;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) nrm_partial[blockIdx.x] = s;
+}
+
+__global__ void pw_reduce_norm(const double* nrm_partial, int nparts, double* nrm) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int p = threadIdx.x; p < nparts; p += blockDim.x) s += nrm_partial[p];
+  // fixed-order: strided partial sums then warp/block tree
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *nrm = sqrt(s);
+}
+
+cudaError_t power_iter_large(const float2* A, int n, int m, long long start, long long stop, double2* v,
+                             double2* u, int max_iter, double rtol, double* result, int num_sms, cudaStream_t st) {
+  const long long width = stop - start;
+  if (width == 1) {
+    // handled by the small kernel path in the caller
+    return cudaErrorInvalidValue;
+  }
+  const int cols_per_cta = 4096;
+  const int nparts = (int)((width + cols_per_cta - 1) / cols_per_cta);
+  const int adj_blocks = num_sms * 4;
+  double2 *partial = nullptr, *w = nullptr;
+  double *scal = nullptr, *nrm_part = nullptr;
+  cudaError_t e = cudaMallocAsync(&partial, sizeof(double2) * (size_t)nparts * n, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&w, sizeof(double2) * n, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&scal, sizeof(double) * 2, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&nrm_part, sizeof(double) * adj_blocks, st);
+  if (e != cudaSuccess) return e;
+  double prev = 0.0, res = 0.0, host[2];
+  double inv = 1.0;  // v holds the unnormalised u after the first iteration; scale folded in
+  bool first = true;
+  for (int it = 0; it < max_iter; ++it) {
+    pw_forward_partial<<<nparts, 256, 0, st>>>(A, n, m, start, width, first ? v : u, inv, cols_per_cta, partial);
+    pw_reduce_w<<<1, 256, 0, st>>>(partial, nparts, n, w, scal);
+    pw_adjoint<<<adj_blocks, 256, 0, st>>>(A, n, m, start, width, w, u, nrm_part);
+    pw_reduce_norm<<<1, 256, 0, st>>>(nrm_part, adj_blocks, scal + 1);
+    e = cudaMemcpyAsync(host, scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) break;
+    const double cur = host[0], nu = host[1];
+    first = false;
+    if (nu == 0.0) {
+      res = 0.0;
+      break;
+    }
+    inv = 1.0 / nu;
+    if (fabs(cur - prev) <= rtol * fmax(cur, 1e-300)) {
+      res = cur;
+      break;
+    }
+    prev = cur;
+    res = prev;
+  }
+  cudaFreeAsync(partial, st);
+  cudaFreeAsync(w, st);
+  cudaFreeAsync(scal, st);
+  cudaFreeAsync(nrm_part, st);
+  *result = res;
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
+}  // namespace tb

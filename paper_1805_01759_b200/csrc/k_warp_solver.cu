@@ -1,0 +1,429 @@
+// Warp-per-pixel proximal-gradient solver: RBPG (paper Alg. 1), FISTA and ISTA.
+//
+// Reference semantics (paths relative to /root/reference/pkg/src/tomobpdn):
+//   rbpg_solve      solver.py:250-338   (block draw, extrapolation, backtracking, monotone accept)
+//   _full_vector_pg solver.py:341-376   (ISTA/FISTA, per-iteration backtracking from alpha0)
+//   soft_threshold  prox.py:82-96, line_search_ok prox.py:107-119, _window_converged solver.py:227-231
+//
+// Layout: the dictionary A (complex64, n x m) is staged ONCE per CTA into shared memory with an
+// odd row stride (conflict-free both for column-lanes in the adjoint and row-lanes in the
+// forward product).  Each warp owns one pixel slot at a time: its iterate x, the extrapolation
+// memory, residual vectors and the F-history ring live in shared memory; the drawn block's
+// y, gradient and candidate live in registers (lanes own columns c = cs + lane + 32 t).
+// Pixels are claimed from a global atomic queue, so retirement of converged pixels and refill
+// happen per warp with no CTA-wide barrier; a pixel's arithmetic does not depend on which
+// warp/CTA/GPU ran it, so results are independent of scheduling and GPU count.
+//
+// Numerics: vectors in fp32 (complex64), every scalar that decides control flow in fp64
+// (objective F, l1 norms, norms in the backtracking test, window stop).  The backtracking test
+// is evaluated in its cancellation-free algebraic form ||A d||^2 <= ||d||^2 / (2 alpha), which is
+// exactly the reference inequality f(z) <= f(y) + Re<grad, d> + ||d||^2/(2 alpha) for quadratic f.
+#include <float.h>
+
+#include "common.cuh"
+#include "solver_params.h"
+
+namespace tb {
+
+template <int MAXT, int MAXQ, bool ASMEM>
+__global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(const SolveParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int n = P.n, m = P.m, ms = P.ms;
+  const int mode = P.mode;
+  const bool rbpg = mode == SOLVER_RBPG;
+
+  float2* As = reinterpret_cast<float2*>(smem);
+  size_t off = ASMEM ? (((size_t)n * ms * sizeof(float2) + 15) & ~(size_t)15) : 0;
+  if (ASMEM) {
+    for (int idx = threadIdx.x; idx < n * m; idx += blockDim.x) {
+      int i = idx / m, c = idx - i * m;
+      As[(size_t)i * ms + c] = __ldg(&P.A[idx]);
+    }
+    __syncthreads();
+  }
+  const size_t per_warp = warp_slot_bytes(n, m);
+  unsigned char* wb = smem + off + (size_t)warp * per_warp;
+  double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA), fp64
+  double2* apv = rv + n;                         // A x_prev (FISTA), fp64
+  float2* xs = reinterpret_cast<float2*>(apv + n);  // x
+  float2* ps = xs + m;                          // prev block values (RBPG) / x_prev (FISTA)
+  float2* zs = ps + m;                          // broadcast buffer for forward products
+  float2* ryv = zs + m;                         // r_y (fp32 copy for the adjoint)
+  float2* bv = ryv + n;                         // b
+  double* ring = reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
+
+  auto Aat = [&](int i, int c) -> float2 {
+    if (ASMEM) return As[(size_t)i * ms + c];
+    return __ldg(&P.A[(size_t)i * m + c]);
+  };
+  // acc[q] += sum_{c < width, zs[c] != 0} A[i][cs + c] * zs[c], fp64 accumulation of exact
+  // fp32 products; zero entries (the sparse bulk of L1 iterates) are skipped warp-uniformly.
+  auto forward = [&](int cs, int width, double2* acc) {
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) acc[q] = make_double2(0.0, 0.0);
+    for (int c = 0; c < width; ++c) {
+      const float2 v = zs[c];
+      if (v.x == 0.f && v.y == 0.f) continue;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int i = lane + 32 * q;
+        if (i < n) {
+          const float2 a = Aat(i, cs + c);
+          acc[q].x = fma((double)a.x, (double)v.x, fma(-(double)a.y, (double)v.y, acc[q].x));
+          acc[q].y = fma((double)a.x, (double)v.y, fma((double)a.y, (double)v.x, acc[q].y));
+        }
+      }
+    }
+  };
+
+  for (;;) {
+    unsigned long long pq = 0;
+    if (lane == 0) pq = atomicAdd(P.queue, 1ull);
+    pq = __shfl_sync(TB_FULL_MASK, pq, 0);
+    if (pq >= (unsigned long long)P.num_pixels) break;
+    const long long p = (long long)pq;
+    const float lam = P.lam[p];
+    const double lamd = (double)lam;
+
+    // ---- initial state: x = 0, prev = 0, r = -b, F0 = ||b||^2 (solver.py:270-276, 349)
+    for (int c = lane; c < m; c += 32) {
+      xs[c] = make_float2(0.f, 0.f);
+      ps[c] = make_float2(0.f, 0.f);
+    }
+    double fb = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      float2 b = P.B[(size_t)p * n + i];
+      bv[i] = b;
+      rv[i] = rbpg ? make_double2(-(double)b.x, -(double)b.y) : make_double2(0.0, 0.0);
+      apv[i] = make_double2(0.0, 0.0);
+      fb += (double)b.x * b.x + (double)b.y * b.y;
+    }
+    double F = warp_sum(fb);
+    double l1 = 0.0;
+    if (lane == 0) ring[0] = F;
+    if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
+    Philox4x64 rng;
+    if (rbpg) philox_init(rng, P.seeds[p], 0ull);
+    int status = STATUS_MAX_ITERS;
+    int iters = 0;
+    bool stopped = false;
+    __syncwarp();
+
+    for (int k = 1; k <= P.total_iters; ++k) {
+      iters = k;
+      // ---- block choice (solver.py:283, 217-219): searchsorted(cdf, u, 'right')
+      int blk = 0, cs = 0, ce = m;
+      if (rbpg) {
+        double u = raw_to_unit(philox_next(rng));
+        int j = 0;
+        while (j < P.num_blocks - 1 && P.cdf[j] <= u) ++j;
+        blk = j;
+        cs = P.blk_start[blk];
+        ce = P.blk_start[blk + 1];
+      }
+      const int width = ce - cs;
+      const double mk = (mode == SOLVER_ISTA) ? 0.0 : (k - 2.0) / (k + 1.0);  // solver.py:222-224
+      const float mkf = (float)mk;
+
+      // ---- extrapolation y = x + m_k (x - prev) (solver.py:288-289, 356)
+      float2 y[MAXT], g[MAXT], z[MAXT];
+      bool any_dy = false;
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        int cl = lane + 32 * t;
+        y[t] = g[t] = z[t] = make_float2(0.f, 0.f);
+        if (cl < width) {
+          float2 xv = xs[cs + cl];
+          float2 pv = ps[cs + cl];
+          float2 yv = xv;
+          if (mode != SOLVER_ISTA) {
+            yv.x = fmaf(mkf, xv.x - pv.x, xv.x);
+            yv.y = fmaf(mkf, xv.y - pv.y, xv.y);
+          }
+          y[t] = yv;
+          float2 dy = make_float2(yv.x - xv.x, yv.y - xv.y);
+          if (rbpg) zs[cl] = dy;
+          any_dy |= (dy.x != 0.f) || (dy.y != 0.f);
+        }
+      }
+      any_dy = __any_sync(TB_FULL_MASK, any_dy);
+      __syncwarp();
+
+      // ---- residual at y (lane = row), fp64: RBPG r_y = r + A_b dy (solver.py:290-291);
+      //      FISTA/ISTA r_y = A y - b with A y = A x + m_k (A x - A x_prev) by linearity.
+      double2 ry[MAXQ], ay[MAXQ];
+      if (rbpg) {
+        double2 acc[MAXQ];
+        if (any_dy) forward(cs, width, acc);
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          const int i = lane + 32 * q;
+          ry[q] = ay[q] = make_double2(0.0, 0.0);
+          if (i < n) {
+            double2 r = rv[i];
+            ry[q] = any_dy ? make_double2(r.x + acc[q].x, r.y + acc[q].y) : r;
+            ryv[i] = make_float2((float)ry[q].x, (float)ry[q].y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          const int i = lane + 32 * q;
+          ry[q] = ay[q] = make_double2(0.0, 0.0);
+          if (i < n) {
+            double2 ax = rv[i], axp = apv[i];
+            float2 b = bv[i];
+            double2 a = ax;
+            if (mode != SOLVER_ISTA) {
+              a.x = fma(mk, ax.x - axp.x, ax.x);
+              a.y = fma(mk, ax.y - axp.y, ax.y);
+            }
+            ay[q] = a;
+            ry[q] = make_double2(a.x - b.x, a.y - b.y);
+            ryv[i] = make_float2((float)ry[q].x, (float)ry[q].y);
+          }
+        }
+      }
+      __syncwarp();
+
+      // ---- block gradient g = 2 A_b^H r_y (solver.py:293, prox.py:77-79)
+      {
+        float2 acc[MAXT];
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
+        for (int i = 0; i < n; ++i) {
+          const float2 r = ryv[i];
+#pragma unroll
+          for (int t = 0; t < MAXT; ++t) {
+            const int cl = lane + 32 * t;
+            if (cl < width) cfma_conj(acc[t], Aat(i, cs + cl), r);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) g[t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
+      }
+
+      // ---- backtracking (solver.py:295-314; prox.py:122-150)
+      const double lip = rbpg ? P.blk_lip[blk] : P.lip_full;
+      double alpha = P.alpha_scale / fmax(lip, 1e-300);
+      bool ok = false;
+      double2 adz[MAXQ];
+      double dzsq = 0.0, l1z = 0.0;
+      for (int trial = 0; trial <= P.cap; ++trial) {
+        const float af = (float)alpha;
+        const float tau = (float)(alpha * lamd);
+        double dzs = 0.0, l1zs = 0.0, ysq = 0.0;
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          int cl = lane + 32 * t;
+          if (cl < width) {
+            float2 v = make_float2(fmaf(-af, g[t].x, y[t].x), fmaf(-af, g[t].y, y[t].y));
+            float mag = hypotf(v.x, v.y);
+            float sc = fmaxf(0.f, 1.f - tau / fmaxf(mag, FLT_MIN));
+            float2 zz = make_float2(v.x * sc, v.y * sc);
+            if (rbpg) z[t] = zz;
+            float2 d = make_float2(zz.x - y[t].x, zz.y - y[t].y);
+            dzs += (double)d.x * d.x + (double)d.y * d.y;
+            l1zs += (double)hypotf(zz.x, zz.y);
+            ysq += (double)y[t].x * y[t].x + (double)y[t].y * y[t].y;
+            zs[cl] = rbpg ? d : zz;
+          }
+        }
+        dzsq = warp_sum(dzs);
+        l1z = warp_sum(l1zs);
+        __syncwarp();
+        forward(cs, width, adz);  // RBPG: A_b dz; FISTA/ISTA: A z
+        __syncwarp();
+        const double rhs = dzsq / (2.0 * alpha);
+        bool pass;
+        if (rbpg) {
+          // ||A_b dz||^2 <= ||dz||^2/(2 alpha) (exact algebra of solver.py:303-310), fp32 slack
+          double l = 0.0;
+#pragma unroll
+          for (int q = 0; q < MAXQ; ++q) l += adz[q].x * adz[q].x + adz[q].y * adz[q].y;
+          l = warp_sum(l);
+          pass = l <= rhs * (1.0 + 1e-5);
+        } else {
+          // A d = A z - A y in fp64; slack covers the fp32 rounding of y and z themselves
+          double l = 0.0;
+#pragma unroll
+          for (int q = 0; q < MAXQ; ++q) {
+            double dx = adz[q].x - ay[q].x, dyy = adz[q].y - ay[q].y;
+            l += dx * dx + dyy * dyy;
+          }
+          l = warp_sum(l);
+          double ny = sqrt(warp_sum(ysq));
+          double slack = 4.0 * 5.9604644775390625e-08 * sqrt(0.5 * lip) * ny;
+          pass = sqrt(l) <= sqrt(rhs) + slack;
+        }
+        if (pass) {
+          ok = true;
+          break;
+        }
+        alpha *= P.c_alpha;
+      }
+      if (!ok) {
+        // RBPG appends F before breaking (solver.py:311-314); ISTA/FISTA do not (solver.py:357-361)
+        if (rbpg) {
+          if (lane == 0) ring[k % (STOP_WINDOW + 1)] = F;
+          if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride + k] = F;
+        }
+        status = STATUS_LINE_SEARCH_FAILURE;
+        stopped = true;
+        break;
+      }
+
+      // ---- update
+      if (rbpg) {
+        // incremental l1, monotone acceptance (solver.py:316-325)
+        double l1xs = 0.0;
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          int cl = lane + 32 * t;
+          if (cl < width) {
+            const float2 xv = xs[cs + cl];
+            l1xs += (double)hypotf(xv.x, xv.y);
+          }
+        }
+        const double l1_new = l1 - warp_sum(l1xs) + l1z;
+        double fz = 0.0;
+        double2 rz[MAXQ];
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          rz[q] = make_double2(ry[q].x + adz[q].x, ry[q].y + adz[q].y);
+          int i = lane + 32 * q;
+          if (i < n) fz += rz[q].x * rz[q].x + rz[q].y * rz[q].y;
+        }
+        fz = warp_sum(fz);
+        const double cand = fz + lamd * l1_new;
+        const bool accept = cand <= F;
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          int cl = lane + 32 * t;
+          if (cl < width) {
+            ps[cs + cl] = xs[cs + cl];
+            if (accept) xs[cs + cl] = z[t];
+          }
+        }
+        if (accept) {
+#pragma unroll
+          for (int q = 0; q < MAXQ; ++q) {
+            int i = lane + 32 * q;
+            if (i < n) rv[i] = rz[q];
+          }
+          l1 = l1_new;
+          F = cand;
+        }
+      } else {
+        // x_prev <- x, x <- z, F = ||A z - b||^2 + lambda ||z||_1 (solver.py:362-364)
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          int cl = lane + 32 * t;
+          if (cl < width) {
+            ps[cl] = xs[cl];
+            xs[cl] = zs[cl];
+          }
+        }
+        double fz = 0.0;
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          int i = lane + 32 * q;
+          if (i < n) {
+            apv[i] = rv[i];
+            rv[i] = adz[q];
+            float2 b = bv[i];
+            double dx = adz[q].x - b.x, dyy = adz[q].y - b.y;
+            fz += dx * dx + dyy * dyy;
+          }
+        }
+        F = warp_sum(fz) + lamd * l1z;
+      }
+      // ---- history, failure and window stop (solver.py:326-336, 366-374)
+      if (lane == 0) ring[k % (STOP_WINDOW + 1)] = F;
+      if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride + k] = F;
+      __syncwarp();
+      if (!isfinite(F)) {
+        status = STATUS_NUMERICAL_FAILURE;
+        stopped = true;
+        break;
+      }
+      if (!P.fixed && k >= STOP_WINDOW) {
+        double ref = ring[(k - STOP_WINDOW) % (STOP_WINDOW + 1)];
+        if (fabs(F - ref) <= P.tol * fmax(fabs(ref), 1e-300)) {
+          status = STATUS_CONVERGED;
+          stopped = true;
+          break;
+        }
+      }
+    }
+    if (!stopped && iters >= STOP_WINDOW) {  // for-else re-check (solver.py:334-336)
+      double ref = ring[(iters - STOP_WINDOW) % (STOP_WINDOW + 1)];
+      if (fabs(F - ref) <= P.tol * fmax(fabs(ref), 1e-300)) status = STATUS_CONVERGED;
+    }
+    __syncwarp();
+    for (int c = lane; c < m; c += 32) P.X[(size_t)p * m + c] = xs[c];
+    if (lane == 0) {
+      P.f_final[p] = F;
+      P.iters[p] = iters;
+      P.status[p] = status;
+    }
+    __syncwarp();
+  }
+}
+
+template <int MAXT, int MAXQ, bool ASMEM>
+static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int grid, cudaStream_t st) {
+  auto k = warp_solver_kernel<MAXT, MAXQ, ASMEM>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, warps * 32, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <int MAXT, bool ASMEM>
+static cudaError_t launch_q(const SolveParams& P, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
+  switch (maxq) {
+    case 1: return launch_t<MAXT, 1, ASMEM>(P, warps, smem, grid, st);
+    case 2: return launch_t<MAXT, 2, ASMEM>(P, warps, smem, grid, st);
+    case 3: return launch_t<MAXT, 3, ASMEM>(P, warps, smem, grid, st);
+    case 4: return launch_t<MAXT, 4, ASMEM>(P, warps, smem, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <bool ASMEM>
+static cudaError_t launch_tq(const SolveParams& P, int maxt, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
+  if (maxt <= 2) return launch_q<2, ASMEM>(P, maxq, warps, smem, grid, st);
+  if (maxt <= 4) return launch_q<4, ASMEM>(P, maxq, warps, smem, grid, st);
+  if (maxt <= 8) return launch_q<8, ASMEM>(P, maxq, warps, smem, grid, st);
+  if (maxt <= 16) return launch_q<16, ASMEM>(P, maxq, warps, smem, grid, st);
+  return cudaErrorInvalidValue;
+}
+
+// Chooses the shared-memory plan and launches a persistent grid (<= resident CTAs).
+cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps) {
+  const int width = P.max_width;
+  int maxt = (width + 31) / 32;
+  maxt = maxt <= 2 ? 2 : maxt <= 4 ? 4 : maxt <= 8 ? 8 : 16;  // template bucket
+  const int maxq = (P.n + 31) / 32;
+  const size_t slot = warp_slot_bytes(P.n, P.m);
+  const size_t a_bytes = ((size_t)P.n * P.ms * sizeof(float2) + 15) & ~(size_t)15;
+  const size_t cap = 227 * 1024;
+  bool asmem = a_bytes + 4 * slot <= cap;
+  size_t avail = cap - (asmem ? a_bytes : 0);
+  int warps = (int)(avail / slot);
+  if (warps > (maxt >= 8 ? 8 : 16)) warps = (maxt >= 8 ? 8 : 16);
+  if (warps < 1) return cudaErrorInvalidValue;
+  size_t smem = (asmem ? a_bytes : 0) + (size_t)warps * slot;
+  long long need = (P.num_pixels + warps - 1) / warps;
+  int grid = num_sms;
+  if (need < grid) grid = (int)need;
+  if (grid < 1) grid = 1;
+  if (used_warps) *used_warps = warps;
+  return asmem ? launch_tq<true>(P, maxt, maxq, warps, smem, grid, st)
+               : launch_tq<false>(P, maxt, maxq, warps, smem, grid, st);
+}
+
+}  // namespace tb

@@ -1,0 +1,47 @@
+// Launchers for the setup and selection kernels (k_setup.cu, k_select.cu).
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include <cuda_runtime.h>
+
+namespace tb {
+
+cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B, long long P, double beta,
+                                  float* lam, int num_sms, cudaStream_t st);
+cudaError_t launch_derive_seeds(uint64_t run_seed, long long first, long long P, uint64_t* seeds, cudaStream_t st);
+cudaError_t launch_power_small(const float2* A, int n, int m, const long long* starts, const long long* stops,
+                               int num_ranges, double2* v, double2* uscratch, int max_iter, double rtol,
+                               double* out_dev, cudaStream_t st);
+cudaError_t power_iter_large(const float2* A, int n, int m, long long start, long long stop, double2* v,
+                             double2* u, int max_iter, double rtol, double* result, int num_sms, cudaStream_t st);
+
+struct SelectParams {
+  const float2* A;
+  int n, m;
+  const float2* X;
+  const float2* B;
+  long long num_pixels;
+  int n_elev, inner, n_axes, msize0, msize1;
+  const double* elev;
+  const double* motion;
+  int k_max, ppsc;
+  int* order;
+  long long* support;
+  double2* amps;
+  double* elevs;
+  double* motion_out;
+  double* scores;
+  int* n_scores;
+  int* err;
+};
+
+// per-warp shared bytes of the selection kernel: profile (double) + argmax (int) + Q[kmax][n]
+__host__ __device__ inline size_t select_warp_bytes(int n, int n_elev, int kmax) {
+  size_t a = ((size_t)n_elev * 12 + 15) & ~(size_t)15;
+  return a + (size_t)kmax * n * 16;
+}
+
+cudaError_t launch_select(const SelectParams& S, int num_sms, cudaStream_t st);
+
+}  // namespace tb

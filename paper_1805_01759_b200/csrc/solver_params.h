@@ -1,0 +1,47 @@
+// Parameter block shared by the host launcher (tb_api.cu) and the solver kernels.
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include <cuda_runtime.h>
+
+namespace tb {
+
+enum { SOLVER_RBPG = 0, SOLVER_FISTA = 1, SOLVER_ISTA = 2 };
+enum { STATUS_CONVERGED = 0, STATUS_MAX_ITERS = 1, STATUS_LINE_SEARCH_FAILURE = 2, STATUS_NUMERICAL_FAILURE = 3 };
+constexpr int STOP_WINDOW = 10;  // solver.py:29
+
+struct SolveParams {
+  const float2* A;  // device [n][m] row-major complex64
+  int n, m, ms;     // ms: odd shared-memory row stride (>= m)
+  int mode;
+  int num_blocks;
+  int max_width;          // widest active column range (block or m)
+  const int* blk_start;   // device [J+1]
+  const double* blk_lip;  // device [J]
+  const double* cdf;      // device [J]
+  double lip_full;
+  int total_iters, fixed, cap;
+  double tol, c_alpha, alpha_scale;
+  const float2* B;
+  const float* lam;
+  const uint64_t* seeds;
+  long long num_pixels;
+  float2* X;
+  double* f_final;
+  double* hist;
+  long long hist_stride;
+  int* iters;
+  int* status;
+  unsigned long long* queue;
+};
+
+// per-warp shared bytes: 2 fp64 n-vectors, x/prev/broadcast (3 m) + 2 fp32 n-vectors, 16-double ring
+__host__ __device__ inline size_t warp_slot_bytes(int n, int m) {
+  size_t b = (size_t)n * 32 + (size_t)(3 * m + 2 * n) * 8 + 16 * 8;
+  return (b + 15) & ~(size_t)15;
+}
+
+cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps);
+
+}  // namespace tb

@@ -1,0 +1,330 @@
+// C ABI implementation (include/tomobpdn_b200.h): context management, validation, launches.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/tomobpdn_b200.h"
+#include "common.cuh"
+#include "setup.h"
+#include "solver_params.h"
+
+struct tb_ctx {
+  int device = 0;
+  int num_sms = 148;
+  int64_t n = 0, m = 0;
+  float2* A = nullptr;  // owned copy, [n][m]
+  // partition
+  int num_blocks = 0;
+  int* blk_start = nullptr;  // device [J+1]
+  double* blk_lip = nullptr; // device [J]
+  double* cdf = nullptr;     // device [J]
+  int max_block_width = 0;
+  double lip_full = 0.0;
+  bool has_partition = false, has_lip = false;
+  unsigned long long* queue = nullptr;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define TB_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess) return fail(TB_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+  } while (0)
+
+extern "C" {
+
+const char* tb_version(void) { return "tomobpdn_b200 0.1.0 sm_100a"; }
+const char* tb_last_error(void) { return g_err.c_str(); }
+
+int tb_ctx_create(int device, const void* dictionary_dev, int64_t n, int64_t m, tb_ctx** out) {
+  if (!out || !dictionary_dev) return fail(TB_ERR_INVALID, "null argument");
+  if (n < 1 || m < 1) return fail(TB_ERR_INVALID, "dictionary must be a 2-d matrix with n, m >= 1 (got %lld x %lld)", (long long)n, (long long)m);
+  if (n > 128) return fail(TB_ERR_INVALID, "n = %lld acquisitions exceeds the supported 128", (long long)n);
+  if (n * m >= (1ll << 31)) return fail(TB_ERR_CAPACITY, "dictionary needs %lld entries, device budget is 2^31", (long long)(n * m));
+  TB_CUDA(cudaSetDevice(device));
+  tb_ctx* c = new tb_ctx();
+  c->device = device;
+  c->n = n;
+  c->m = m;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaMalloc(&c->A, sizeof(float2) * n * m);
+  if (e == cudaSuccess) e = cudaMemcpy(c->A, dictionary_dev, sizeof(float2) * n * m, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&c->queue, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    cudaFree(c->A);
+    delete c;
+    return fail(TB_ERR_CUDA, "tb_ctx_create: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return TB_OK;
+}
+
+int tb_ctx_destroy(tb_ctx* c) {
+  if (!c) return TB_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->A);
+  cudaFree(c->blk_start);
+  cudaFree(c->blk_lip);
+  cudaFree(c->cdf);
+  cudaFree(c->queue);
+  delete c;
+  return TB_OK;
+}
+
+int tb_spectral_sq_norms(tb_ctx* c, int32_t num_ranges, const int64_t* starts, const int64_t* stops,
+                         const void* v0_dev, int32_t max_iter, double rtol, double* sigma2_host, void* stream) {
+  if (!c || !starts || !stops || !v0_dev || !sigma2_host) return fail(TB_ERR_INVALID, "null argument");
+  if (num_ranges < 1) return fail(TB_ERR_INVALID, "num_ranges must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  TB_CUDA(cudaSetDevice(c->device));
+  long long total = 0;
+  std::vector<long long> s(num_ranges), e(num_ranges);
+  for (int r = 0; r < num_ranges; ++r) {
+    s[r] = starts[r];
+    e[r] = stops[r];
+    if (s[r] < 0 || e[r] > c->m || e[r] <= s[r]) return fail(TB_ERR_INVALID, "range %d [%lld, %lld) invalid for m = %lld", r, s[r], e[r], (long long)c->m);
+    total += e[r] - s[r];
+  }
+  double2 *v = nullptr, *u = nullptr;
+  double* out = nullptr;
+  TB_CUDA(cudaMallocAsync(&v, sizeof(double2) * total, st));
+  TB_CUDA(cudaMallocAsync(&u, sizeof(double2) * total, st));
+  TB_CUDA(cudaMallocAsync(&out, sizeof(double) * num_ranges, st));
+  TB_CUDA(cudaMemcpyAsync(v, v0_dev, sizeof(double2) * total, cudaMemcpyDeviceToDevice, st));
+  // small ranges on one CTA each (whole loop on device), wide ranges host-driven multi-CTA
+  const long long small_limit = 1ll << 22;
+  std::vector<long long> ss, se;
+  std::vector<int> small_idx;
+  std::vector<long long> offs(num_ranges);
+  long long off = 0;
+  for (int r = 0; r < num_ranges; ++r) {
+    offs[r] = off;
+    off += e[r] - s[r];
+  }
+  // the small kernel indexes v by its own concatenation; run it over a compacted copy
+  for (int r = 0; r < num_ranges; ++r)
+    if ((e[r] - s[r]) * c->n <= small_limit || e[r] - s[r] == 1) {
+      ss.push_back(s[r]);
+      se.push_back(e[r]);
+      small_idx.push_back(r);
+    }
+  std::vector<double> hres(num_ranges, 0.0);
+  if (!small_idx.empty()) {
+    long long tot_small = 0;
+    for (size_t k = 0; k < ss.size(); ++k) tot_small += se[k] - ss[k];
+    double2 *vs = nullptr, *us = nullptr;
+    double* os = nullptr;
+    TB_CUDA(cudaMallocAsync(&vs, sizeof(double2) * tot_small, st));
+    TB_CUDA(cudaMallocAsync(&us, sizeof(double2) * tot_small, st));
+    TB_CUDA(cudaMallocAsync(&os, sizeof(double) * ss.size(), st));
+    long long o2 = 0;
+    for (size_t k = 0; k < ss.size(); ++k) {
+      int r = small_idx[k];
+      TB_CUDA(cudaMemcpyAsync(vs + o2, v + offs[r], sizeof(double2) * (e[r] - s[r]), cudaMemcpyDeviceToDevice, st));
+      o2 += e[r] - s[r];
+    }
+    TB_CUDA(tb::launch_power_small(c->A, (int)c->n, (int)c->m, ss.data(), se.data(), (int)ss.size(), vs, us, max_iter, rtol, os, st));
+    std::vector<double> hs(ss.size());
+    TB_CUDA(cudaMemcpyAsync(hs.data(), os, sizeof(double) * ss.size(), cudaMemcpyDeviceToHost, st));
+    TB_CUDA(cudaStreamSynchronize(st));
+    for (size_t k = 0; k < ss.size(); ++k) hres[small_idx[k]] = hs[k];
+    cudaFreeAsync(vs, st);
+    cudaFreeAsync(us, st);
+    cudaFreeAsync(os, st);
+  }
+  for (int r = 0; r < num_ranges; ++r) {
+    if ((e[r] - s[r]) * c->n <= small_limit || e[r] - s[r] == 1) continue;
+    TB_CUDA(tb::power_iter_large(c->A, (int)c->n, (int)c->m, s[r], e[r], v + offs[r], u + offs[r], max_iter, rtol, &hres[r], c->num_sms, st));
+  }
+  TB_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(v, st);
+  cudaFreeAsync(u, st);
+  cudaFreeAsync(out, st);
+  for (int r = 0; r < num_ranges; ++r) sigma2_host[r] = hres[r];
+  return TB_OK;
+}
+
+int tb_set_partition(tb_ctx* c, int32_t J, const int64_t* starts, const int64_t* stops, const double* lip) {
+  if (!c || !starts || !stops || !lip) return fail(TB_ERR_INVALID, "null argument");
+  if (J < 1 || J > c->m) return fail(TB_ERR_INVALID, "num_blocks must lie in [1, %lld], got %d", (long long)c->m, J);
+  std::vector<int> bs(J + 1);
+  double total = 0.0;
+  int maxw = 0;
+  for (int j = 0; j < J; ++j) {
+    if (starts[j] != (j == 0 ? 0 : stops[j - 1]) || stops[j] <= starts[j]) return fail(TB_ERR_INVALID, "blocks must be contiguous, disjoint, non-empty");
+    if (!(lip[j] >= 0.0) || lip[j] != lip[j] || lip[j] > 1.7e308) return fail(TB_ERR_INVALID, "Lipschitz constants must be finite and >= 0");
+    bs[j] = (int)starts[j];
+    total += lip[j];
+    int w = (int)(stops[j] - starts[j]);
+    if (w > maxw) maxw = w;
+  }
+  if (stops[J - 1] != c->m) return fail(TB_ERR_INVALID, "blocks must cover all %lld columns", (long long)c->m);
+  if (!(total > 0.0)) return fail(TB_ERR_INVALID, "at least one block must have positive Lipschitz");
+  bs[J] = (int)c->m;
+  // numpy Generator.choice: p = L / sum(L) (solver.py:156-160), cdf = cumsum(p), cdf /= cdf[-1]
+  std::vector<double> p(J), cdf(J);
+  for (int j = 0; j < J; ++j) p[j] = lip[j] / total;
+  double acc = 0.0;
+  for (int j = 0; j < J; ++j) {
+    acc += p[j];
+    cdf[j] = acc;
+  }
+  const double last = cdf[J - 1];
+  for (int j = 0; j < J; ++j) cdf[j] /= last;
+  TB_CUDA(cudaSetDevice(c->device));
+  cudaFree(c->blk_start);
+  cudaFree(c->blk_lip);
+  cudaFree(c->cdf);
+  c->blk_start = nullptr;
+  c->blk_lip = c->cdf = nullptr;
+  TB_CUDA(cudaMalloc(&c->blk_start, sizeof(int) * (J + 1)));
+  TB_CUDA(cudaMalloc(&c->blk_lip, sizeof(double) * J));
+  TB_CUDA(cudaMalloc(&c->cdf, sizeof(double) * J));
+  TB_CUDA(cudaMemcpy(c->blk_start, bs.data(), sizeof(int) * (J + 1), cudaMemcpyHostToDevice));
+  TB_CUDA(cudaMemcpy(c->blk_lip, lip, sizeof(double) * J, cudaMemcpyHostToDevice));
+  TB_CUDA(cudaMemcpy(c->cdf, cdf.data(), sizeof(double) * J, cudaMemcpyHostToDevice));
+  c->num_blocks = J;
+  c->max_block_width = maxw;
+  c->has_partition = true;
+  return TB_OK;
+}
+
+int tb_set_lipschitz(tb_ctx* c, double lip) {
+  if (!c) return fail(TB_ERR_INVALID, "null context");
+  if (!(lip >= 0.0) || lip > 1.7e308) return fail(TB_ERR_INVALID, "Lipschitz constant must be finite and >= 0");
+  c->lip_full = lip;
+  c->has_lip = true;
+  return TB_OK;
+}
+
+int tb_default_lambda(tb_ctx* c, const void* pixels, int64_t P, double beta, float* lam, void* stream) {
+  if (!c || (P > 0 && (!pixels || !lam))) return fail(TB_ERR_INVALID, "null argument");
+  if (P < 0) return fail(TB_ERR_INVALID, "num_pixels must be >= 0");
+  TB_CUDA(cudaSetDevice(c->device));
+  TB_CUDA(tb::launch_default_lambda(c->A, (int)c->n, (int)c->m, (const float2*)pixels, P, beta, lam, c->num_sms, (cudaStream_t)stream));
+  return TB_OK;
+}
+
+int tb_derive_seeds(uint64_t run_seed, int64_t first, int64_t P, uint64_t* seeds, void* stream) {
+  if (P < 0 || (P > 0 && !seeds)) return fail(TB_ERR_INVALID, "invalid seeds arguments");
+  TB_CUDA(tb::launch_derive_seeds(run_seed, first, P, seeds, (cudaStream_t)stream));
+  return TB_OK;
+}
+
+int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const float* lam,
+             const uint64_t* seeds, int64_t P, void* x, double* f_final, double* hist, int64_t hist_stride,
+             int32_t* iters, int32_t* status, void* stream) {
+  if (!c || !cfg) return fail(TB_ERR_INVALID, "null argument");
+  if (P < 0) return fail(TB_ERR_INVALID, "num_pixels must be >= 0");
+  if (P == 0) return TB_OK;
+  if (!pixels || !lam || !x || !f_final || !iters || !status) return fail(TB_ERR_INVALID, "null buffer");
+  if (solver != TB_SOLVER_RBPG && solver != TB_SOLVER_FISTA && solver != TB_SOLVER_ISTA) return fail(TB_ERR_INVALID, "unknown solver %d", solver);
+  if (cfg->max_iters < 1) return fail(TB_ERR_INVALID, "max_iters must be >= 1, got %d", cfg->max_iters);
+  if (!(cfg->tol > 0.0)) return fail(TB_ERR_INVALID, "tol must be > 0");
+  if (!(cfg->c_alpha > 0.0 && cfg->c_alpha < 1.0)) return fail(TB_ERR_INVALID, "c_alpha must lie in (0, 1)");
+  if (!(cfg->alpha_init_scale > 0.0)) return fail(TB_ERR_INVALID, "alpha_init_scale must be > 0");
+  if (cfg->backtrack_cap < 0) return fail(TB_ERR_INVALID, "backtrack_cap must be >= 0");
+  const int total = cfg->fixed_iters > 0 ? cfg->fixed_iters : cfg->max_iters;
+  if (hist && hist_stride < total + 1) return fail(TB_ERR_INVALID, "hist_stride %lld < iterations + 1", (long long)hist_stride);
+  tb::SolveParams S{};
+  S.A = c->A;
+  S.n = (int)c->n;
+  S.m = (int)c->m;
+  S.ms = (int)(c->m | 1);
+  S.mode = solver;
+  if (solver == TB_SOLVER_RBPG) {
+    if (!c->has_partition) return fail(TB_ERR_INVALID, "RBPG needs tb_set_partition first");
+    if (cfg->num_blocks != c->num_blocks) return fail(TB_ERR_INVALID, "config num_blocks %d != partition %d", cfg->num_blocks, c->num_blocks);
+    if (!seeds) return fail(TB_ERR_INVALID, "RBPG needs per-pixel seeds");
+    S.max_width = c->max_block_width;
+  } else {
+    if (!c->has_lip) return fail(TB_ERR_INVALID, "ISTA/FISTA need tb_set_lipschitz first");
+    S.max_width = (int)c->m;
+  }
+  if ((S.max_width + 31) / 32 > 16) return fail(TB_ERR_CAPACITY, "active width %d exceeds the warp solver's 512 columns", S.max_width);
+  S.num_blocks = c->num_blocks;
+  S.blk_start = c->blk_start;
+  S.blk_lip = c->blk_lip;
+  S.cdf = c->cdf;
+  S.lip_full = c->lip_full;
+  S.total_iters = total;
+  S.fixed = cfg->fixed_iters > 0;
+  S.cap = cfg->backtrack_cap;
+  S.tol = cfg->tol;
+  S.c_alpha = cfg->c_alpha;
+  S.alpha_scale = cfg->alpha_init_scale;
+  S.B = (const float2*)pixels;
+  S.lam = lam;
+  S.seeds = seeds;
+  S.num_pixels = P;
+  S.X = (float2*)x;
+  S.f_final = f_final;
+  S.hist = hist;
+  S.hist_stride = hist_stride;
+  S.iters = iters;
+  S.status = status;
+  S.queue = c->queue;
+  cudaStream_t st = (cudaStream_t)stream;
+  TB_CUDA(cudaSetDevice(c->device));
+  TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
+  int warps = 0;
+  TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
+  return TB_OK;
+}
+
+int tb_select(tb_ctx* c, const void* x, const void* pixels, int64_t P, int32_t n_elev, int32_t n_axes,
+              const int32_t* msizes, const double* elev, const double* motion, int32_t k_max, int32_t ppsc,
+              int32_t* order, int64_t* support, void* amps, double* elevs, double* motion_out, double* scores,
+              int32_t* n_scores, int32_t* err, void* stream) {
+  if (!c) return fail(TB_ERR_INVALID, "null context");
+  if (k_max < 1) return fail(TB_ERR_INVALID, "k_max must be >= 1, got %d", k_max);
+  if (k_max > 8) return fail(TB_ERR_INVALID, "k_max %d exceeds the supported 8", k_max);
+  if (n_axes < 0 || n_axes > 2) return fail(TB_ERR_INVALID, "1 elevation + at most 2 motion axes supported");
+  long long inner = 1;
+  for (int a = 0; a < n_axes; ++a) inner *= msizes[a];
+  if ((long long)n_elev * inner != c->m) return fail(TB_ERR_INVALID, "grid size %lld != dictionary columns %lld", (long long)n_elev * inner, (long long)c->m);
+  if (P == 0) return TB_OK;
+  tb::SelectParams S{};
+  S.A = c->A;
+  S.n = (int)c->n;
+  S.m = (int)c->m;
+  S.X = (const float2*)x;
+  S.B = (const float2*)pixels;
+  S.num_pixels = P;
+  S.n_elev = n_elev;
+  S.inner = (int)inner;
+  S.n_axes = n_axes;
+  S.msize0 = n_axes >= 1 ? msizes[0] : 1;
+  S.msize1 = n_axes >= 2 ? msizes[1] : 1;
+  S.elev = elev;
+  S.motion = motion;
+  S.k_max = k_max;
+  S.ppsc = ppsc;
+  S.order = order;
+  S.support = (long long*)support;
+  S.amps = (double2*)amps;
+  S.elevs = elevs;
+  S.motion_out = motion_out;
+  S.scores = scores;
+  S.n_scores = n_scores;
+  S.err = err;
+  TB_CUDA(cudaSetDevice(c->device));
+  TB_CUDA(tb::launch_select(S, c->num_sms, (cudaStream_t)stream));
+  return TB_OK;
+}
+
+}  // extern "C"

@@ -212,8 +212,8 @@ def make_config(cfg: int, num_pixels: int | None = None, seed: int = 2018) -> Sy
             ref = mag[:, 0]
         gains = mag * np.exp(1j * ph)
         sigma2 = ref**2 * 10.0 ** (-snr / 10.0)
-        pos, gains, sigma2 = pos[:pc], gains[:pc], sigma2[:pc]
-        chunks.append(_pixels_from_truth(a128, pos, gains, sigma2, _rng(seed, 16 + cfg, c0 // _CHUNK)))
+        chunks.append(_pixels_from_truth(a128, pos, gains, sigma2, _rng(seed, 16 + cfg, c0 // _CHUNK))[:pc])
+        pos = pos[:pc]
         if p_total <= 65536:
             supports.extend([sorted(int(v) for v in row if v >= 0) for row in pos])
     pixels = np.concatenate(chunks, axis=0) if chunks else np.zeros((0, n), np.complex64)
