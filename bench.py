@@ -1,0 +1,304 @@
+"""Benchmark: pixels/s solved to tolerance (complex64 L1-LS) on BASELINE.json config 2.
+
+A step = one pass of the hot path over the whole synthetic batch already resident in HBM:
+lambda rule (0.1 max|A^H b|) -> per-pixel RBPG seeds -> batched solve (max_iters=500, tol=1e-6)
+-> SL1MMER selection.  Prints ONE JSON line (rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 2] [--backend rbpg|fista|ista] [--pixels P]
+
+Multi-GPU (torchrun, one rank per GPU): each rank solves its own full batch (pixel ids offset by
+rank, no collective on the data path) -> weak scaling; value = all pixels / max-over-ranks time.
+``--impl reference`` times the reference algorithm (the fp64 oracle port of the reference
+code path, all host cores, process pool as in cli.py:136-144) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pixels/sec solved to tolerance (complex64 L1-LS) and % of roofline, 1/2/4/8 GPU"
+UNIT = "pixels/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--backend", default="rbpg", choices=["rbpg", "fista", "ista"])
+    ap.add_argument("--pixels", type=int, default=None)
+    ap.add_argument("--cpu-sample", type=int, default=None, help="pixels per CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def flops_per_pixel_iteration(backend, n, m, num_blocks):
+    """Algorithmic FLOPs: one adjoint + one forward product, 8 real flops per complex MAC."""
+    return 16.0 * n * m / (num_blocks if backend == "rbpg" else 1)
+
+
+def cpu_baseline(batch, backend, sample, lam, seeds, workers, solver_kw):
+    """The reference algorithm (oracle port, per-solve power iterations as in solver.py:267/344)."""
+    from oracle import batch as OB
+
+    a = batch.dictionary.astype(np.complex128)
+    t0 = time.perf_counter()
+    res = OB.run(a, batch.pixels[:sample], lam[:sample], backend, seeds=seeds[:sample], workers=workers, **solver_kw)
+    wall = time.perf_counter() - t0
+    its = np.array([r["iterations"] for r in res])
+    return sample / wall, wall, its
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 6]
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[3 + j].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def fp32_peak():
+    """FP32 FFMA peak: MEASURED_PEAKS.json has no SIMT figure; use the committed probe result."""
+    path = os.path.join(ROOT, "profiles", "peaks_fp32.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["ffma_fp32_tflops"]), "profiles/peaks_fp32.json (tools/peak_probe.cu FFMA burst on B200)"
+    except Exception:
+        return 70.78, "tools/peak_probe.cu FFMA burst on B200 (70.78 TFLOP/s, round 1)"
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1805_01759_b200.synth import lambda_from_beta, make_config
+    from oracle import tomo_oracle as O
+
+    cores = os.cpu_count() or 1
+    sample = args.cpu_sample or max(cores * 24, 64)
+    batch = make_config(args.config, num_pixels=sample)
+    lam = lambda_from_beta(batch.dictionary, batch.pixels, 0.1)
+    seeds = np.array([O.derive_seed(2018, p) for p in range(sample)], dtype=np.uint64)
+    kw = dict(max_iters=500, tol=1e-6, num_blocks=8)
+    vals = []
+    for step in range(args.warmup + args.steps):
+        v, wall, its = cpu_baseline(batch, args.backend, sample, lam, seeds, cores, kw)
+        if step >= args.warmup:
+            vals.append(v)
+    value = float(np.median(vals))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * sample / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (BASELINE.json config, seeded)", "impl": "reference",
+        "config": {"workload": f"cfg{args.config}", "backend": args.backend, "pixels_per_step": sample, "max_iters": 500, "tol": 1e-6},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": f"first {sample} pixels of cfg{args.config}, {args.backend}, process pool x{cores}, per-solve power iterations as solver.py:267/344"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    import paper_1805_01759_b200 as tb
+    from paper_1805_01759_b200.synth import make_config
+
+    batch = make_config(args.config, num_pixels=args.pixels)
+    P, n, m = batch.num_pixels, batch.n, batch.m
+    d = tb.Dictionary(batch.dictionary, device=dev)
+    grid = batch.grid
+    scfg = tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8, seed=2018)
+    pcfg = tb.PipelineConfig(solver=scfg, backend=args.backend, k_max=batch.k_max)
+    first_id = rank * P
+    pix_dev = torch.from_numpy(batch.pixels).to(dev)
+    pix_host = torch.from_numpy(batch.pixels).pin_memory()
+    # per-dictionary setup (power iterations) outside the timed region, like a resident service
+    if args.backend == "rbpg":
+        d.partition(scfg.num_blocks)
+    else:
+        d.lipschitz()
+    stream = torch.cuda.current_stream(dev)
+
+    def step(pixels):
+        return tb.pipeline_batch(d, pixels, grid, pcfg, beta=0.1, first_pixel_id=first_id)
+
+    for _ in range(args.warmup):
+        est = step(pix_dev)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ks, ke = [], []
+    iters_total = 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        lam = d.default_lambda(pix_dev, 0.1)
+        seeds = d.derive_seeds(scfg.seed, P, first_id) if args.backend == "rbpg" else None
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sol = d.solve(pix_dev, lam, scfg, args.backend, seeds=seeds)
+        b.record(stream)
+        est = tb.select_batch(d, sol.x_hat, pix_dev, grid, batch.k_max)
+        ks.append(a)
+        ke.append(b)
+        iters_total += sol.iterations  # device tensor accumulate (no sync)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    kms = [x.elapsed_time(y) for x, y in zip(ks, ke)]
+    pix_iters = float(iters_total.double().sum().item()) if hasattr(iters_total, "double") else 0.0
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * P * args.steps / (ms / 1000.0)
+
+    # ---- roofline of the dominant kernel (the solver launch), achieved from live CUDA events
+    flop_pi = flops_per_pixel_iteration(args.backend, n, m, scfg.num_blocks)
+    kernel_ms = float(np.mean(kms))
+    achieved = pix_iters / args.steps * flop_pi / (kernel_ms / 1000.0) / 1e12
+    peak, peak_src = fp32_peak()
+
+    # ---- end to end through the public API with host buffers (pinned H2D in, D2H results out)
+    e2e_ms = []
+    h2d = pix_host.numel() * pix_host.element_size()
+    d2h = 0
+    for s in range(max(2, min(args.steps, 3)) + 1):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        px = pix_host.to(dev, non_blocking=True)
+        est = step(px)
+        outs = [est.model_order, est.support, est.amplitudes, est.elevations, est.solution.objective_final, est.solution.iterations, est.solution.status]
+        host = [o.to("cpu", non_blocking=True) for o in outs]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        d2h = sum(o.numel() * o.element_size() for o in outs)
+        if s > 0:
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e_step = float(np.median(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
+    e2e_value = world * P / (e2e_step / 1000.0)
+    st = est.solution.status.cpu().numpy()
+    its = est.solution.iterations.cpu().numpy()
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c64 (fp64 scalars/residuals)", "data": "synthetic (BASELINE.json config 2 shapes and distributions, seeded)",
+            "config": {
+                "workload": f"cfg{args.config}", "n": n, "m": m, "pixels_per_gpu": P, "backend": args.backend, "num_blocks": 8,
+                "max_iters": 500, "tol": 1e-6, "lambda": "0.1*max|A^H b|", "k_max": batch.k_max, "parallelism": f"pixel-sharded x{world}, no collective",
+                "l2": "inputs (B = %d MB) and x_hat output exceed the 126 MB L2; no explicit flush" % (P * n * 8 // 2**20),
+                "step": "lambda + seeds + solve + select, whole batch",
+            },
+            "roofline": {
+                "bound": "fp32", "kernel": "warp_solver_kernel", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic": f"{flop_pi:.0f} flop per pixel-iteration (16 n m{'/J' if args.backend == 'rbpg' else ''}) x {pix_iters / args.steps:.4g} pixel-iterations per launch",
+                "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms_per_step,
+            },
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
+            "gpu_launches": args.steps * (4 if args.backend == "rbpg" else 3),
+            "clocks": clk,
+            "solver_stats": {"mean_iterations": float(its.mean()), "converged_frac": float((st == 0).mean()), "max_iters_frac": float((st == 1).mean())},
+        }
+        if not args.no_cpu_baseline:
+            from oracle import tomo_oracle as O
+            from paper_1805_01759_b200.synth import lambda_from_beta
+
+            cores = os.cpu_count() or 1
+            sample = args.cpu_sample or max(cores * 32, 64)
+            lam_h = lambda_from_beta(batch.dictionary, batch.pixels[:sample], 0.1)
+            seeds_h = np.array([O.derive_seed(2018, p) for p in range(sample)], dtype=np.uint64)
+            v, wall, _ = cpu_baseline(batch, args.backend, sample, lam_h, seeds_h, cores, dict(max_iters=500, tol=1e-6, num_blocks=8))
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": f"first {sample} pixels of cfg{args.config}, {args.backend}, process pool x{cores}, {wall:.1f} s wall, per-solve power iterations as solver.py:267/344"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -25,14 +25,13 @@
 
 namespace tb {
 
-template <int MAXT, int MAXQ, bool ASMEM>
+template <bool RB, int MAXT, int MAXQ, bool ASMEM>
 __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int n = P.n, m = P.m, ms = P.ms;
-  const int mode = P.mode;
-  const bool rbpg = mode == SOLVER_RBPG;
+  const bool ista = P.mode == SOLVER_ISTA;
 
   float2* As = reinterpret_cast<float2*>(smem);
   size_t off = ASMEM ? (((size_t)n * ms * sizeof(float2) + 15) & ~(size_t)15) : 0;
@@ -43,36 +42,36 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
     }
     __syncthreads();
   }
-  const size_t per_warp = warp_slot_bytes(n, m);
+  const size_t per_warp = warp_slot_bytes(n, m, P.max_width);
   unsigned char* wb = smem + off + (size_t)warp * per_warp;
-  double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA), fp64
-  double2* apv = rv + n;                         // A x_prev (FISTA), fp64
-  float2* xs = reinterpret_cast<float2*>(apv + n);  // x
-  float2* ps = xs + m;                          // prev block values (RBPG) / x_prev (FISTA)
-  float2* zs = ps + m;                          // broadcast buffer for forward products
-  float2* ryv = zs + m;                         // r_y (fp32 copy for the adjoint)
-  float2* bv = ryv + n;                         // b
+  double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA)
+  double2* apv = rv + n;                         // A x_prev (FISTA)
+  double2* xs = apv + n;                         // x (fp64 iterate)
+  double2* ps = xs + m;                          // prev block values (RBPG) / x_prev (FISTA)
+  double2* zs = ps + m;                          // broadcast buffer for forward products [max_width]
+  float2* ryv = reinterpret_cast<float2*>(zs + P.max_width);  // r_y rounded for the adjoint
+  float2* bv = ryv + n;                          // b
   double* ring = reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
 
   auto Aat = [&](int i, int c) -> float2 {
     if (ASMEM) return As[(size_t)i * ms + c];
     return __ldg(&P.A[(size_t)i * m + c]);
   };
-  // acc[q] += sum_{c < width, zs[c] != 0} A[i][cs + c] * zs[c], fp64 accumulation of exact
-  // fp32 products; zero entries (the sparse bulk of L1 iterates) are skipped warp-uniformly.
+  // acc[q] += sum_{c < width, zs[c] != 0} A[i][cs + c] * zs[c] in fp64; exact zeros (the sparse
+  // bulk of L1 iterates) are skipped warp-uniformly.
   auto forward = [&](int cs, int width, double2* acc) {
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q) acc[q] = make_double2(0.0, 0.0);
     for (int c = 0; c < width; ++c) {
-      const float2 v = zs[c];
-      if (v.x == 0.f && v.y == 0.f) continue;
+      const double2 v = zs[c];
+      if (v.x == 0.0 && v.y == 0.0) continue;
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
         const int i = lane + 32 * q;
         if (i < n) {
           const float2 a = Aat(i, cs + c);
-          acc[q].x = fma((double)a.x, (double)v.x, fma(-(double)a.y, (double)v.y, acc[q].x));
-          acc[q].y = fma((double)a.x, (double)v.y, fma((double)a.y, (double)v.x, acc[q].y));
+          acc[q].x = fma((double)a.x, v.x, fma(-(double)a.y, v.y, acc[q].x));
+          acc[q].y = fma((double)a.x, v.y, fma((double)a.y, v.x, acc[q].y));
         }
       }
     }
@@ -84,19 +83,18 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
     pq = __shfl_sync(TB_FULL_MASK, pq, 0);
     if (pq >= (unsigned long long)P.num_pixels) break;
     const long long p = (long long)pq;
-    const float lam = P.lam[p];
-    const double lamd = (double)lam;
+    const double lamd = (double)P.lam[p];
 
     // ---- initial state: x = 0, prev = 0, r = -b, F0 = ||b||^2 (solver.py:270-276, 349)
     for (int c = lane; c < m; c += 32) {
-      xs[c] = make_float2(0.f, 0.f);
-      ps[c] = make_float2(0.f, 0.f);
+      xs[c] = make_double2(0.0, 0.0);
+      ps[c] = make_double2(0.0, 0.0);
     }
     double fb = 0.0;
     for (int i = lane; i < n; i += 32) {
       float2 b = P.B[(size_t)p * n + i];
       bv[i] = b;
-      rv[i] = rbpg ? make_double2(-(double)b.x, -(double)b.y) : make_double2(0.0, 0.0);
+      rv[i] = RB ? make_double2(-(double)b.x, -(double)b.y) : make_double2(0.0, 0.0);
       apv[i] = make_double2(0.0, 0.0);
       fb += (double)b.x * b.x + (double)b.y * b.y;
     }
@@ -105,7 +103,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
     if (lane == 0) ring[0] = F;
     if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
     Philox4x64 rng;
-    if (rbpg) philox_init(rng, P.seeds[p], 0ull);
+    if (RB) philox_init(rng, P.seeds[p], 0ull);
     int status = STATUS_MAX_ITERS;
     int iters = 0;
     bool stopped = false;
@@ -115,7 +113,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       iters = k;
       // ---- block choice (solver.py:283, 217-219): searchsorted(cdf, u, 'right')
       int blk = 0, cs = 0, ce = m;
-      if (rbpg) {
+      if (RB) {
         double u = raw_to_unit(philox_next(rng));
         int j = 0;
         while (j < P.num_blocks - 1 && P.cdf[j] <= u) ++j;
@@ -124,37 +122,40 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
         ce = P.blk_start[blk + 1];
       }
       const int width = ce - cs;
-      const double mk = (mode == SOLVER_ISTA) ? 0.0 : (k - 2.0) / (k + 1.0);  // solver.py:222-224
-      const float mkf = (float)mk;
+      const double mk = ista ? 0.0 : (k - 2.0) / (k + 1.0);  // solver.py:222-224
 
       // ---- extrapolation y = x + m_k (x - prev) (solver.py:288-289, 356)
-      float2 y[MAXT], g[MAXT], z[MAXT];
+      double2 y[MAXT];
+      float2 g[MAXT];
+      double2 z[RB ? MAXT : 1];
       bool any_dy = false;
 #pragma unroll
       for (int t = 0; t < MAXT; ++t) {
-        int cl = lane + 32 * t;
-        y[t] = g[t] = z[t] = make_float2(0.f, 0.f);
+        const int cl = lane + 32 * t;
+        y[t] = make_double2(0.0, 0.0);
         if (cl < width) {
-          float2 xv = xs[cs + cl];
-          float2 pv = ps[cs + cl];
-          float2 yv = xv;
-          if (mode != SOLVER_ISTA) {
-            yv.x = fmaf(mkf, xv.x - pv.x, xv.x);
-            yv.y = fmaf(mkf, xv.y - pv.y, xv.y);
+          const double2 xv = xs[cs + cl];
+          const double2 pv = ps[cs + cl];
+          double2 yv = xv;
+          if (!ista) {
+            yv.x = fma(mk, xv.x - pv.x, xv.x);
+            yv.y = fma(mk, xv.y - pv.y, xv.y);
           }
           y[t] = yv;
-          float2 dy = make_float2(yv.x - xv.x, yv.y - xv.y);
-          if (rbpg) zs[cl] = dy;
-          any_dy |= (dy.x != 0.f) || (dy.y != 0.f);
+          if (RB) {
+            const double2 dy = make_double2(yv.x - xv.x, yv.y - xv.y);
+            zs[cl] = dy;
+            any_dy |= (dy.x != 0.0) || (dy.y != 0.0);
+          }
         }
       }
-      any_dy = __any_sync(TB_FULL_MASK, any_dy);
+      if (RB) any_dy = __any_sync(TB_FULL_MASK, any_dy);
       __syncwarp();
 
       // ---- residual at y (lane = row), fp64: RBPG r_y = r + A_b dy (solver.py:290-291);
       //      FISTA/ISTA r_y = A y - b with A y = A x + m_k (A x - A x_prev) by linearity.
       double2 ry[MAXQ], ay[MAXQ];
-      if (rbpg) {
+      if (RB) {
         double2 acc[MAXQ];
         if (any_dy) forward(cs, width, acc);
 #pragma unroll
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
           const int i = lane + 32 * q;
           ry[q] = ay[q] = make_double2(0.0, 0.0);
           if (i < n) {
-            double2 r = rv[i];
+            const double2 r = rv[i];
             ry[q] = any_dy ? make_double2(r.x + acc[q].x, r.y + acc[q].y) : r;
             ryv[i] = make_float2((float)ry[q].x, (float)ry[q].y);
           }
@@ -173,10 +174,10 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
           const int i = lane + 32 * q;
           ry[q] = ay[q] = make_double2(0.0, 0.0);
           if (i < n) {
-            double2 ax = rv[i], axp = apv[i];
-            float2 b = bv[i];
+            const double2 ax = rv[i], axp = apv[i];
+            const float2 b = bv[i];
             double2 a = ax;
-            if (mode != SOLVER_ISTA) {
+            if (!ista) {
               a.x = fma(mk, ax.x - axp.x, ax.x);
               a.y = fma(mk, ax.y - axp.y, ax.y);
             }
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       }
       __syncwarp();
 
-      // ---- block gradient g = 2 A_b^H r_y (solver.py:293, prox.py:77-79)
+      // ---- block gradient g = 2 A_b^H r_y (solver.py:293, prox.py:77-79), fp32 products
       {
         float2 acc[MAXT];
 #pragma unroll
@@ -205,30 +206,33 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
         for (int t = 0; t < MAXT; ++t) g[t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
       }
 
-      // ---- backtracking (solver.py:295-314; prox.py:122-150)
-      const double lip = rbpg ? P.blk_lip[blk] : P.lip_full;
+      // ---- backtracking (solver.py:295-314; prox.py:122-150), prox step in fp64
+      const double lip = RB ? P.blk_lip[blk] : P.lip_full;
       double alpha = P.alpha_scale / fmax(lip, 1e-300);
       bool ok = false;
       double2 adz[MAXQ];
       double dzsq = 0.0, l1z = 0.0;
       for (int trial = 0; trial <= P.cap; ++trial) {
-        const float af = (float)alpha;
-        const float tau = (float)(alpha * lamd);
-        double dzs = 0.0, l1zs = 0.0, ysq = 0.0;
+        const double tau = alpha * lamd;
+        const double tau2 = tau * tau;
+        double dzs = 0.0, l1zs = 0.0;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
-          int cl = lane + 32 * t;
+          const int cl = lane + 32 * t;
           if (cl < width) {
-            float2 v = make_float2(fmaf(-af, g[t].x, y[t].x), fmaf(-af, g[t].y, y[t].y));
-            float mag = hypotf(v.x, v.y);
-            float sc = fmaxf(0.f, 1.f - tau / fmaxf(mag, FLT_MIN));
-            float2 zz = make_float2(v.x * sc, v.y * sc);
-            if (rbpg) z[t] = zz;
-            float2 d = make_float2(zz.x - y[t].x, zz.y - y[t].y);
-            dzs += (double)d.x * d.x + (double)d.y * d.y;
-            l1zs += (double)hypotf(zz.x, zz.y);
-            ysq += (double)y[t].x * y[t].x + (double)y[t].y * y[t].y;
-            zs[cl] = rbpg ? d : zz;
+            const double2 v = make_double2(fma(-alpha, (double)g[t].x, y[t].x), fma(-alpha, (double)g[t].y, y[t].y));
+            const double mag2 = fma(v.x, v.x, v.y * v.y);
+            double2 zz = make_double2(0.0, 0.0);
+            if (mag2 > tau2) {  // soft_threshold: zero iff |v| <= tau (prox.py:82-96)
+              const double mag = sqrt(mag2);
+              const double sc = 1.0 - tau / mag;
+              zz = make_double2(v.x * sc, v.y * sc);
+              l1zs += mag * sc;
+            }
+            if (RB) z[t] = zz;
+            const double2 d = make_double2(zz.x - y[t].x, zz.y - y[t].y);
+            dzs += fma(d.x, d.x, d.y * d.y);
+            zs[cl] = RB ? d : zz;
           }
         }
         dzsq = warp_sum(dzs);
@@ -237,25 +241,21 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
         forward(cs, width, adz);  // RBPG: A_b dz; FISTA/ISTA: A z
         __syncwarp();
         const double rhs = dzsq / (2.0 * alpha);
+        double l = 0.0, na = 0.0;
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          // quadratic-bound test in its exact algebraic form ||A d||^2 <= ||d||^2 / (2 alpha)
+          const double dx = RB ? adz[q].x : adz[q].x - ay[q].x;
+          const double dyy = RB ? adz[q].y : adz[q].y - ay[q].y;
+          l += dx * dx + dyy * dyy;
+          if (!RB) na += fabs(adz[q].x) + fabs(adz[q].y) + fabs(ay[q].x) + fabs(ay[q].y);
+        }
+        l = warp_sum(l);
         bool pass;
-        if (rbpg) {
-          // ||A_b dz||^2 <= ||dz||^2/(2 alpha) (exact algebra of solver.py:303-310), fp32 slack
-          double l = 0.0;
-#pragma unroll
-          for (int q = 0; q < MAXQ; ++q) l += adz[q].x * adz[q].x + adz[q].y * adz[q].y;
-          l = warp_sum(l);
-          pass = l <= rhs * (1.0 + 1e-5);
+        if (RB) {
+          pass = l <= rhs * (1.0 + 1e-9);
         } else {
-          // A d = A z - A y in fp64; slack covers the fp32 rounding of y and z themselves
-          double l = 0.0;
-#pragma unroll
-          for (int q = 0; q < MAXQ; ++q) {
-            double dx = adz[q].x - ay[q].x, dyy = adz[q].y - ay[q].y;
-            l += dx * dx + dyy * dyy;
-          }
-          l = warp_sum(l);
-          double ny = sqrt(warp_sum(ysq));
-          double slack = 4.0 * 5.9604644775390625e-08 * sqrt(0.5 * lip) * ny;
+          const double slack = 1e-12 * warp_sum(na);  // fp64 rounding of the A z - A y difference
           pass = sqrt(l) <= sqrt(rhs) + slack;
         }
         if (pass) {
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       }
       if (!ok) {
         // RBPG appends F before breaking (solver.py:311-314); ISTA/FISTA do not (solver.py:357-361)
-        if (rbpg) {
+        if (RB) {
           if (lane == 0) ring[k % (STOP_WINDOW + 1)] = F;
           if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride + k] = F;
         }
@@ -276,15 +276,15 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       }
 
       // ---- update
-      if (rbpg) {
+      if (RB) {
         // incremental l1, monotone acceptance (solver.py:316-325)
         double l1xs = 0.0;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
-          int cl = lane + 32 * t;
+          const int cl = lane + 32 * t;
           if (cl < width) {
-            const float2 xv = xs[cs + cl];
-            l1xs += (double)hypotf(xv.x, xv.y);
+            const double2 xv = xs[cs + cl];
+            if (xv.x != 0.0 || xv.y != 0.0) l1xs += sqrt(fma(xv.x, xv.x, xv.y * xv.y));
           }
         }
         const double l1_new = l1 - warp_sum(l1xs) + l1z;
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
           rz[q] = make_double2(ry[q].x + adz[q].x, ry[q].y + adz[q].y);
-          int i = lane + 32 * q;
+          const int i = lane + 32 * q;
           if (i < n) fz += rz[q].x * rz[q].x + rz[q].y * rz[q].y;
         }
         fz = warp_sum(fz);
@@ -301,16 +301,16 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
         const bool accept = cand <= F;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
-          int cl = lane + 32 * t;
+          const int cl = lane + 32 * t;
           if (cl < width) {
             ps[cs + cl] = xs[cs + cl];
-            if (accept) xs[cs + cl] = z[t];
+            if (accept) xs[cs + cl] = z[RB ? t : 0];
           }
         }
         if (accept) {
 #pragma unroll
           for (int q = 0; q < MAXQ; ++q) {
-            int i = lane + 32 * q;
+            const int i = lane + 32 * q;
             if (i < n) rv[i] = rz[q];
           }
           l1 = l1_new;
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
         // x_prev <- x, x <- z, F = ||A z - b||^2 + lambda ||z||_1 (solver.py:362-364)
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
-          int cl = lane + 32 * t;
+          const int cl = lane + 32 * t;
           if (cl < width) {
             ps[cl] = xs[cl];
             xs[cl] = zs[cl];
@@ -329,12 +329,12 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
         double fz = 0.0;
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
-          int i = lane + 32 * q;
+          const int i = lane + 32 * q;
           if (i < n) {
             apv[i] = rv[i];
             rv[i] = adz[q];
-            float2 b = bv[i];
-            double dx = adz[q].x - b.x, dyy = adz[q].y - b.y;
+            const float2 b = bv[i];
+            const double dx = adz[q].x - b.x, dyy = adz[q].y - b.y;
             fz += dx * dx + dyy * dyy;
           }
         }
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
         break;
       }
       if (!P.fixed && k >= STOP_WINDOW) {
-        double ref = ring[(k - STOP_WINDOW) % (STOP_WINDOW + 1)];
+        const double ref = ring[(k - STOP_WINDOW) % (STOP_WINDOW + 1)];
         if (fabs(F - ref) <= P.tol * fmax(fabs(ref), 1e-300)) {
           status = STATUS_CONVERGED;
           stopped = true;
@@ -359,11 +359,14 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       }
     }
     if (!stopped && iters >= STOP_WINDOW) {  // for-else re-check (solver.py:334-336)
-      double ref = ring[(iters - STOP_WINDOW) % (STOP_WINDOW + 1)];
+      const double ref = ring[(iters - STOP_WINDOW) % (STOP_WINDOW + 1)];
       if (fabs(F - ref) <= P.tol * fmax(fabs(ref), 1e-300)) status = STATUS_CONVERGED;
     }
     __syncwarp();
-    for (int c = lane; c < m; c += 32) P.X[(size_t)p * m + c] = xs[c];
+    for (int c = lane; c < m; c += 32) {
+      const double2 xv = xs[c];
+      P.X[(size_t)p * m + c] = make_float2((float)xv.x, (float)xv.y);
+    }
     if (lane == 0) {
       P.f_final[p] = F;
       P.iters[p] = iters;
@@ -373,32 +376,31 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
   }
 }
 
-template <int MAXT, int MAXQ, bool ASMEM>
+template <bool RB, int MAXT, int MAXQ, bool ASMEM>
 static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int grid, cudaStream_t st) {
-  auto k = warp_solver_kernel<MAXT, MAXQ, ASMEM>;
+  auto k = warp_solver_kernel<RB, MAXT, MAXQ, ASMEM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, warps * 32, smem, st>>>(P);
   return cudaGetLastError();
 }
 
-template <int MAXT, bool ASMEM>
+template <bool RB, int MAXT, bool ASMEM>
 static cudaError_t launch_q(const SolveParams& P, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
   switch (maxq) {
-    case 1: return launch_t<MAXT, 1, ASMEM>(P, warps, smem, grid, st);
-    case 2: return launch_t<MAXT, 2, ASMEM>(P, warps, smem, grid, st);
-    case 3: return launch_t<MAXT, 3, ASMEM>(P, warps, smem, grid, st);
-    case 4: return launch_t<MAXT, 4, ASMEM>(P, warps, smem, grid, st);
+    case 1: return launch_t<RB, MAXT, 1, ASMEM>(P, warps, smem, grid, st);
+    case 2: return launch_t<RB, MAXT, 2, ASMEM>(P, warps, smem, grid, st);
+    case 4: return launch_t<RB, MAXT, 4, ASMEM>(P, warps, smem, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-template <bool ASMEM>
+template <bool RB, bool ASMEM>
 static cudaError_t launch_tq(const SolveParams& P, int maxt, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
-  if (maxt <= 2) return launch_q<2, ASMEM>(P, maxq, warps, smem, grid, st);
-  if (maxt <= 4) return launch_q<4, ASMEM>(P, maxq, warps, smem, grid, st);
-  if (maxt <= 8) return launch_q<8, ASMEM>(P, maxq, warps, smem, grid, st);
-  if (maxt <= 16) return launch_q<16, ASMEM>(P, maxq, warps, smem, grid, st);
+  if (maxt <= 2) return launch_q<RB, 2, ASMEM>(P, maxq, warps, smem, grid, st);
+  if (maxt <= 4) return launch_q<RB, 4, ASMEM>(P, maxq, warps, smem, grid, st);
+  if (maxt <= 8) return launch_q<RB, 8, ASMEM>(P, maxq, warps, smem, grid, st);
+  if (maxt <= 16) return launch_q<RB, 16, ASMEM>(P, maxq, warps, smem, grid, st);
   return cudaErrorInvalidValue;
 }
 
@@ -407,14 +409,16 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   const int width = P.max_width;
   int maxt = (width + 31) / 32;
   maxt = maxt <= 2 ? 2 : maxt <= 4 ? 4 : maxt <= 8 ? 8 : 16;  // template bucket
-  const int maxq = (P.n + 31) / 32;
-  const size_t slot = warp_slot_bytes(P.n, P.m);
+  int maxq = (P.n + 31) / 32;
+  maxq = maxq <= 1 ? 1 : maxq <= 2 ? 2 : 4;
+  const size_t slot = warp_slot_bytes(P.n, P.m, P.max_width);
   const size_t a_bytes = ((size_t)P.n * P.ms * sizeof(float2) + 15) & ~(size_t)15;
   const size_t cap = 227 * 1024;
+  const int max_warps = maxt >= 8 ? 8 : 16;
   bool asmem = a_bytes + 4 * slot <= cap;
   size_t avail = cap - (asmem ? a_bytes : 0);
   int warps = (int)(avail / slot);
-  if (warps > (maxt >= 8 ? 8 : 16)) warps = (maxt >= 8 ? 8 : 16);
+  if (warps > max_warps) warps = max_warps;
   if (warps < 1) return cudaErrorInvalidValue;
   size_t smem = (asmem ? a_bytes : 0) + (size_t)warps * slot;
   long long need = (P.num_pixels + warps - 1) / warps;
@@ -422,8 +426,9 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   if (need < grid) grid = (int)need;
   if (grid < 1) grid = 1;
   if (used_warps) *used_warps = warps;
-  return asmem ? launch_tq<true>(P, maxt, maxq, warps, smem, grid, st)
-               : launch_tq<false>(P, maxt, maxq, warps, smem, grid, st);
+  const bool rb = P.mode == SOLVER_RBPG;
+  if (rb) return asmem ? launch_tq<true, true>(P, maxt, maxq, warps, smem, grid, st) : launch_tq<true, false>(P, maxt, maxq, warps, smem, grid, st);
+  return asmem ? launch_tq<false, true>(P, maxt, maxq, warps, smem, grid, st) : launch_tq<false, false>(P, maxt, maxq, warps, smem, grid, st);
 }
 
 }  // namespace tb

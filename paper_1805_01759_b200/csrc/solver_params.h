@@ -36,9 +36,10 @@ struct SolveParams {
   unsigned long long* queue;
 };
 
-// per-warp shared bytes: 2 fp64 n-vectors, x/prev/broadcast (3 m) + 2 fp32 n-vectors, 16-double ring
-__host__ __device__ inline size_t warp_slot_bytes(int n, int m) {
-  size_t b = (size_t)n * 32 + (size_t)(3 * m + 2 * n) * 8 + 16 * 8;
+// per-warp shared bytes: 2 fp64 n-vectors, fp64 x / prev (2 m) + broadcast buffer (width),
+// 2 fp32 n-vectors, 16-double ring
+__host__ __device__ inline size_t warp_slot_bytes(int n, int m, int width) {
+  size_t b = (size_t)n * 32 + (size_t)(2 * m + width) * 16 + (size_t)n * 16 + 16 * 8;
   return (b + 15) & ~(size_t)15;
 }
 

@@ -228,7 +228,12 @@ class Dictionary:
     def __init__(self, a, device=None):
         torch = _torch()
         lib = _lib.load()
-        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        if device is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        elif isinstance(device, torch.device):
+            dev = device if device.index is not None else torch.device("cuda", torch.cuda.current_device())
+        else:
+            dev = torch.device("cuda", int(device))
         if isinstance(a, torch.Tensor):
             at = a.to(device=dev, dtype=torch.complex64).contiguous()
         else:

@@ -168,7 +168,7 @@ def test_determinism_and_order_independence(tb, cfg1):
     batch = make_config(1, num_pixels=512)
     d = tb.Dictionary(batch.dictionary)
     lam = d.default_lambda(batch.pixels, 0.1)
-    seeds = d.derive_seeds(7, 512)
+    seeds = d.derive_seeds(7, 512).view(torch.int64)
     cfg = tb.SolverConfig(max_iters=500, tol=1e-6)
     for backend in ("rbpg", "fista"):
         r1 = d.solve(batch.pixels, lam, cfg, backend, seeds=seeds)
