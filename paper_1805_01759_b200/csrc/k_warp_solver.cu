@@ -26,7 +26,7 @@
 namespace tb {
 
 template <bool RB, int MAXT, int MAXQ, bool ASMEM>
-__global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(const SolveParams P) {
+__global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -42,7 +42,22 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
     }
     __syncthreads();
   }
-  const size_t per_warp = warp_slot_bytes(n, m, P.max_width);
+  // per-CTA block tables (RBPG): choice CDF, alpha0 = scale / L_i (solver.py:295), block starts
+  const int J = RB ? P.num_blocks : 1;
+  double* s_cdf = reinterpret_cast<double*>(smem + off);
+  double* s_alpha0 = s_cdf + J;
+  int* s_bstart = reinterpret_cast<int*>(s_alpha0 + J);
+  if (RB) {
+    for (int j = threadIdx.x; j < J; j += blockDim.x) {
+      s_cdf[j] = P.cdf[j];
+      s_alpha0[j] = P.alpha_scale / fmax(P.blk_lip[j], 1e-300);
+    }
+    for (int j = threadIdx.x; j <= J; j += blockDim.x) s_bstart[j] = P.blk_start[j];
+  }
+  __syncthreads();
+  off += block_table_bytes(J);
+  const double alpha0_full = P.alpha_scale / fmax(P.lip_full, 1e-300);  // solver.py:345
+  const size_t per_warp = warp_slot_bytes(n, m, P.max_width, J);
   unsigned char* wb = smem + off + (size_t)warp * per_warp;
   double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA)
   double2* apv = rv + n;                         // A x_prev (FISTA)
@@ -52,29 +67,41 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
   float2* ryv = reinterpret_cast<float2*>(zs + P.max_width);  // r_y rounded for the adjoint
   float2* bv = ryv + n;                          // b
   double* ring = reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
+  double* l1blk = ring + 16;                     // RBPG: sum |x_b| per block (updated on accept)
 
   auto Aat = [&](int i, int c) -> float2 {
     if (ASMEM) return As[(size_t)i * ms + c];
     return __ldg(&P.A[(size_t)i * m + c]);
   };
-  // acc[q] += sum_{c < width, zs[c] != 0} A[i][cs + c] * zs[c] in fp64; exact zeros (the sparse
-  // bulk of L1 iterates) are skipped warp-uniformly.
-  auto forward = [&](int cs, int width, double2* acc) {
+  // acc[q] += sum over the nonzero entries of zs (bitmask per 32-column chunk, built with
+  // __ballot_sync) of A[i][cs + c] * zs[c], fp64 accumulation.  L1 iterates and their steps are
+  // sparse, so only the few surviving columns are visited (warp-uniform loop).
+  auto forward = [&](int cs, const unsigned* masks, double2* acc) {
+    const float2* arow[MAXQ];
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) acc[q] = make_double2(0.0, 0.0);
-    for (int c = 0; c < width; ++c) {
-      const double2 v = zs[c];
-      if (v.x == 0.0 && v.y == 0.0) continue;
+    for (int q = 0; q < MAXQ; ++q) {
+      acc[q] = make_double2(0.0, 0.0);
+      const int i = min(lane + 32 * q, n - 1);
+      arow[q] = ASMEM ? As + i * ms + cs : P.A + (size_t)i * m + cs;
+    }
 #pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
-        const int i = lane + 32 * q;
-        if (i < n) {
-          const float2 a = Aat(i, cs + c);
+    for (int t = 0; t < MAXT; ++t) {
+      unsigned mk = masks[t];
+      while (mk) {
+        const int c = (__ffs(mk) - 1) + 32 * t;
+        mk &= mk - 1;
+        const double2 v = zs[c];
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          const float2 a = ASMEM ? arow[q][c] : __ldg(arow[q] + c);
           acc[q].x = fma((double)a.x, v.x, fma(-(double)a.y, v.y, acc[q].x));
           acc[q].y = fma((double)a.x, v.y, fma((double)a.y, v.x, acc[q].y));
         }
       }
     }
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q)
+      if (lane + 32 * q >= n) acc[q] = make_double2(0.0, 0.0);
   };
 
   for (;;) {
@@ -100,6 +127,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
     }
     double F = warp_sum(fb);
     double l1 = 0.0;
+    if (RB)
+      for (int j = lane; j < J; j += 32) l1blk[j] = 0.0;
     if (lane == 0) ring[0] = F;
     if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
     Philox4x64 rng;
@@ -116,23 +145,25 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       if (RB) {
         double u = raw_to_unit(philox_next(rng));
         int j = 0;
-        while (j < P.num_blocks - 1 && P.cdf[j] <= u) ++j;
+        while (j < J - 1 && s_cdf[j] <= u) ++j;
         blk = j;
-        cs = P.blk_start[blk];
-        ce = P.blk_start[blk + 1];
+        cs = s_bstart[blk];
+        ce = s_bstart[blk + 1];
       }
       const int width = ce - cs;
-      const double mk = ista ? 0.0 : (k - 2.0) / (k + 1.0);  // solver.py:222-224
+      const double mk = ista ? 0.0 : P.mk[k];  // (k-2)/(k+1), host table (solver.py:222-224)
 
       // ---- extrapolation y = x + m_k (x - prev) (solver.py:288-289, 356)
       double2 y[MAXT];
       float2 g[MAXT];
       double2 z[RB ? MAXT : 1];
+      unsigned masks[MAXT];
       bool any_dy = false;
 #pragma unroll
       for (int t = 0; t < MAXT; ++t) {
         const int cl = lane + 32 * t;
         y[t] = make_double2(0.0, 0.0);
+        bool nz = false;
         if (cl < width) {
           const double2 xv = xs[cs + cl];
           const double2 pv = ps[cs + cl];
@@ -145,11 +176,12 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
           if (RB) {
             const double2 dy = make_double2(yv.x - xv.x, yv.y - xv.y);
             zs[cl] = dy;
-            any_dy |= (dy.x != 0.0) || (dy.y != 0.0);
+            nz = (dy.x != 0.0) || (dy.y != 0.0);
           }
         }
+        masks[t] = __ballot_sync(TB_FULL_MASK, nz);
+        any_dy |= masks[t] != 0u;
       }
-      if (RB) any_dy = __any_sync(TB_FULL_MASK, any_dy);
       __syncwarp();
 
       // ---- residual at y (lane = row), fp64: RBPG r_y = r + A_b dy (solver.py:290-291);
@@ -157,7 +189,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       double2 ry[MAXQ], ay[MAXQ];
       if (RB) {
         double2 acc[MAXQ];
-        if (any_dy) forward(cs, width, acc);
+        if (any_dy) forward(cs, masks, acc);
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
           const int i = lane + 32 * q;
@@ -194,12 +226,14 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
         float2 acc[MAXT];
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
-        for (int i = 0; i < n; ++i) {
+        const float2* acol = ASMEM ? As + cs + lane : P.A + cs + lane;
+        const int stride = ASMEM ? ms : m;
+        int aoff = 0;
+        for (int i = 0; i < n; ++i, aoff += stride) {
           const float2 r = ryv[i];
 #pragma unroll
           for (int t = 0; t < MAXT; ++t) {
-            const int cl = lane + 32 * t;
-            if (cl < width) cfma_conj(acc[t], Aat(i, cs + cl), r);
+            if (lane + 32 * t < width) cfma_conj(acc[t], ASMEM ? acol[aoff + 32 * t] : __ldg(acol + aoff + 32 * t), r);
           }
         }
 #pragma unroll
@@ -207,18 +241,18 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       }
 
       // ---- backtracking (solver.py:295-314; prox.py:122-150), prox step in fp64
-      const double lip = RB ? P.blk_lip[blk] : P.lip_full;
-      double alpha = P.alpha_scale / fmax(lip, 1e-300);
+      double alpha = RB ? s_alpha0[blk] : alpha0_full;
       bool ok = false;
       double2 adz[MAXQ];
-      double dzsq = 0.0, l1z = 0.0;
+      double l1z = 0.0, fzs = 0.0;
       for (int trial = 0; trial <= P.cap; ++trial) {
         const double tau = alpha * lamd;
         const double tau2 = tau * tau;
-        double dzs = 0.0, l1zs = 0.0;
+        double red[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // |d|^2, |z|, ||A d||^2, f(z), scale (FISTA)
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
           const int cl = lane + 32 * t;
+          bool nz = false;
           if (cl < width) {
             const double2 v = make_double2(fma(-alpha, (double)g[t].x, y[t].x), fma(-alpha, (double)g[t].y, y[t].y));
             const double mag2 = fma(v.x, v.x, v.y * v.y);
@@ -227,36 +261,51 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
               const double mag = sqrt(mag2);
               const double sc = 1.0 - tau / mag;
               zz = make_double2(v.x * sc, v.y * sc);
-              l1zs += mag * sc;
+              red[1] += mag * sc;
             }
             if (RB) z[t] = zz;
             const double2 d = make_double2(zz.x - y[t].x, zz.y - y[t].y);
-            dzs += fma(d.x, d.x, d.y * d.y);
-            zs[cl] = RB ? d : zz;
+            red[0] += fma(d.x, d.x, d.y * d.y);
+            const double2 w = RB ? d : zz;
+            zs[cl] = w;
+            nz = (w.x != 0.0) || (w.y != 0.0);
           }
+          masks[t] = __ballot_sync(TB_FULL_MASK, nz);
         }
-        dzsq = warp_sum(dzs);
-        l1z = warp_sum(l1zs);
         __syncwarp();
-        forward(cs, width, adz);  // RBPG: A_b dz; FISTA/ISTA: A z
-        __syncwarp();
-        const double rhs = dzsq / (2.0 * alpha);
-        double l = 0.0, na = 0.0;
+        forward(cs, masks, adz);  // RBPG: A_b dz; FISTA/ISTA: A z
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
-          // quadratic-bound test in its exact algebraic form ||A d||^2 <= ||d||^2 / (2 alpha)
-          const double dx = RB ? adz[q].x : adz[q].x - ay[q].x;
-          const double dyy = RB ? adz[q].y : adz[q].y - ay[q].y;
-          l += dx * dx + dyy * dyy;
-          if (!RB) na += fabs(adz[q].x) + fabs(adz[q].y) + fabs(ay[q].x) + fabs(ay[q].y);
+          const int i = lane + 32 * q;
+          if (i < n) {
+            // quadratic-bound test in its exact algebraic form ||A d||^2 <= ||d||^2 / (2 alpha)
+            if (RB) {
+              red[2] += adz[q].x * adz[q].x + adz[q].y * adz[q].y;
+              const double rx = ry[q].x + adz[q].x, ryy = ry[q].y + adz[q].y;
+              red[3] += rx * rx + ryy * ryy;
+            } else {
+              const double dx = adz[q].x - ay[q].x, dyy = adz[q].y - ay[q].y;
+              red[2] += dx * dx + dyy * dyy;
+              const float2 b = bv[i];
+              const double fx = adz[q].x - b.x, fy = adz[q].y - b.y;
+              red[3] += fx * fx + fy * fy;
+              red[4] += fabs(adz[q].x) + fabs(adz[q].y) + fabs(ay[q].x) + fabs(ay[q].y);
+            }
+          }
         }
-        l = warp_sum(l);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+          for (int r = 0; r < (RB ? 4 : 5); ++r) red[r] += __shfl_xor_sync(TB_FULL_MASK, red[r], o);
+        }
+        __syncwarp();
+        l1z = red[1];
+        fzs = red[3];
         bool pass;
         if (RB) {
-          pass = l <= rhs * (1.0 + 1e-9);
+          pass = red[2] * (2.0 * alpha) <= red[0] * (1.0 + 1e-9);  // ||A d||^2 <= ||d||^2/(2 alpha)
         } else {
-          const double slack = 1e-12 * warp_sum(na);  // fp64 rounding of the A z - A y difference
-          pass = sqrt(l) <= sqrt(rhs) + slack;
+          pass = sqrt(red[2]) <= sqrt(red[0] / (2.0 * alpha)) + 1e-12 * red[4];  // fp64 rounding of A z - A y
         }
         if (pass) {
           ok = true;
@@ -278,26 +327,11 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
       // ---- update
       if (RB) {
         // incremental l1, monotone acceptance (solver.py:316-325)
-        double l1xs = 0.0;
-#pragma unroll
-        for (int t = 0; t < MAXT; ++t) {
-          const int cl = lane + 32 * t;
-          if (cl < width) {
-            const double2 xv = xs[cs + cl];
-            if (xv.x != 0.0 || xv.y != 0.0) l1xs += sqrt(fma(xv.x, xv.x, xv.y * xv.y));
-          }
-        }
-        const double l1_new = l1 - warp_sum(l1xs) + l1z;
-        double fz = 0.0;
+        const double l1_new = l1 - l1blk[blk] + l1z;
         double2 rz[MAXQ];
 #pragma unroll
-        for (int q = 0; q < MAXQ; ++q) {
-          rz[q] = make_double2(ry[q].x + adz[q].x, ry[q].y + adz[q].y);
-          const int i = lane + 32 * q;
-          if (i < n) fz += rz[q].x * rz[q].x + rz[q].y * rz[q].y;
-        }
-        fz = warp_sum(fz);
-        const double cand = fz + lamd * l1_new;
+        for (int q = 0; q < MAXQ; ++q) rz[q] = make_double2(ry[q].x + adz[q].x, ry[q].y + adz[q].y);
+        const double cand = fzs + lamd * l1_new;
         const bool accept = cand <= F;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
@@ -315,6 +349,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
           }
           l1 = l1_new;
           F = cand;
+          if (lane == 0) l1blk[blk] = l1z;
         }
       } else {
         // x_prev <- x, x <- z, F = ||A z - b||^2 + lambda ||z||_1 (solver.py:362-364)
@@ -326,19 +361,15 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 512) warp_solver_kernel(cons
             xs[cl] = zs[cl];
           }
         }
-        double fz = 0.0;
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
           const int i = lane + 32 * q;
           if (i < n) {
             apv[i] = rv[i];
             rv[i] = adz[q];
-            const float2 b = bv[i];
-            const double dx = adz[q].x - b.x, dyy = adz[q].y - b.y;
-            fz += dx * dx + dyy * dyy;
           }
         }
-        F = warp_sum(fz) + lamd * l1z;
+        F = fzs + lamd * l1z;
       }
       // ---- history, failure and window stop (solver.py:326-336, 366-374)
       if (lane == 0) ring[k % (STOP_WINDOW + 1)] = F;
@@ -411,16 +442,18 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   maxt = maxt <= 2 ? 2 : maxt <= 4 ? 4 : maxt <= 8 ? 8 : 16;  // template bucket
   int maxq = (P.n + 31) / 32;
   maxq = maxq <= 1 ? 1 : maxq <= 2 ? 2 : 4;
-  const size_t slot = warp_slot_bytes(P.n, P.m, P.max_width);
+  const int J = P.mode == SOLVER_RBPG ? P.num_blocks : 1;
+  const size_t slot = warp_slot_bytes(P.n, P.m, P.max_width, J);
+  const size_t tables = block_table_bytes(J);
   const size_t a_bytes = ((size_t)P.n * P.ms * sizeof(float2) + 15) & ~(size_t)15;
   const size_t cap = 227 * 1024;
-  const int max_warps = maxt >= 8 ? 8 : 16;
-  bool asmem = a_bytes + 4 * slot <= cap;
-  size_t avail = cap - (asmem ? a_bytes : 0);
+  const int max_warps = maxt >= 8 ? 8 : 12;
+  bool asmem = a_bytes + tables + 4 * slot <= cap;
+  size_t avail = cap - tables - (asmem ? a_bytes : 0);
   int warps = (int)(avail / slot);
   if (warps > max_warps) warps = max_warps;
   if (warps < 1) return cudaErrorInvalidValue;
-  size_t smem = (asmem ? a_bytes : 0) + (size_t)warps * slot;
+  size_t smem = (asmem ? a_bytes : 0) + tables + (size_t)warps * slot;
   long long need = (P.num_pixels + warps - 1) / warps;
   int grid = num_sms;
   if (need < grid) grid = (int)need;

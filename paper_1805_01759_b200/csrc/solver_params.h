@@ -20,6 +20,7 @@ struct SolveParams {
   const int* blk_start;   // device [J+1]
   const double* blk_lip;  // device [J]
   const double* cdf;      // device [J]
+  const double* mk;       // device [total_iters + 1]: (k-2)/(k+1)
   double lip_full;
   int total_iters, fixed, cap;
   double tol, c_alpha, alpha_scale;
@@ -37,9 +38,14 @@ struct SolveParams {
 };
 
 // per-warp shared bytes: 2 fp64 n-vectors, fp64 x / prev (2 m) + broadcast buffer (width),
-// 2 fp32 n-vectors, 16-double ring
-__host__ __device__ inline size_t warp_slot_bytes(int n, int m, int width) {
-  size_t b = (size_t)n * 32 + (size_t)(2 * m + width) * 16 + (size_t)n * 16 + 16 * 8;
+// 2 fp32 n-vectors, 16-double ring, J-double per-block l1 cache
+__host__ __device__ inline size_t warp_slot_bytes(int n, int m, int width, int J) {
+  size_t b = (size_t)n * 32 + (size_t)(2 * m + width) * 16 + (size_t)n * 16 + 16 * 8 + (size_t)J * 8;
+  return (b + 15) & ~(size_t)15;
+}
+// per-CTA block tables: cdf, alpha0 (J doubles each) + J+1 block starts
+__host__ __device__ inline size_t block_table_bytes(int J) {
+  size_t b = (size_t)J * 16 + (size_t)(J + 1) * 4;
   return (b + 15) & ~(size_t)15;
 }
 

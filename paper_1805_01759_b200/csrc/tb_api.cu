@@ -25,9 +25,34 @@ struct tb_ctx {
   double lip_full = 0.0;
   bool has_partition = false, has_lip = false;
   unsigned long long* queue = nullptr;
+  double* mk = nullptr;  // momentum table (k-2)/(k+1), k = 0..mk_len-1
+  int mk_len = 0;
 };
 
 static thread_local std::string g_err;
+
+// numpy's pairwise summation for float64 (the `lip.sum()` of solver.py:156), so the block
+// probabilities and the choice CDF are bit-identical to the reference's.
+static double numpy_pairwise_sum(const double* a, long long n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (long long i = 0; i < n; ++i) res += a[i];
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    long long i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  long long n2 = n / 2;
+  n2 -= n2 % 8;
+  return numpy_pairwise_sum(a, n2) + numpy_pairwise_sum(a + n2, n - n2);
+}
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -81,6 +106,7 @@ int tb_ctx_destroy(tb_ctx* c) {
   cudaFree(c->blk_lip);
   cudaFree(c->cdf);
   cudaFree(c->queue);
+  cudaFree(c->mk);
   delete c;
   return TB_OK;
 }
@@ -168,11 +194,11 @@ int tb_set_partition(tb_ctx* c, int32_t J, const int64_t* starts, const int64_t*
     if (starts[j] != (j == 0 ? 0 : stops[j - 1]) || stops[j] <= starts[j]) return fail(TB_ERR_INVALID, "blocks must be contiguous, disjoint, non-empty");
     if (!(lip[j] >= 0.0) || lip[j] != lip[j] || lip[j] > 1.7e308) return fail(TB_ERR_INVALID, "Lipschitz constants must be finite and >= 0");
     bs[j] = (int)starts[j];
-    total += lip[j];
     int w = (int)(stops[j] - starts[j]);
     if (w > maxw) maxw = w;
   }
   if (stops[J - 1] != c->m) return fail(TB_ERR_INVALID, "blocks must cover all %lld columns", (long long)c->m);
+  total = numpy_pairwise_sum(lip, J);
   if (!(total > 0.0)) return fail(TB_ERR_INVALID, "at least one block must have positive Lipschitz");
   bs[J] = (int)c->m;
   // numpy Generator.choice: p = L / sum(L) (solver.py:156-160), cdf = cumsum(p), cdf /= cdf[-1]
@@ -280,6 +306,18 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   S.queue = c->queue;
   cudaStream_t st = (cudaStream_t)stream;
   TB_CUDA(cudaSetDevice(c->device));
+  if (c->mk_len < total + 1) {
+    // theta_k = 2/(k+1) collapsed to m_k = (k-2)/(k+1) (solver.py:222-224), IEEE double division
+    std::vector<double> h(total + 1);
+    for (int k = 0; k <= total; ++k) h[k] = (k - 2.0) / (k + 1.0);
+    TB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(c->mk);
+    c->mk = nullptr;
+    TB_CUDA(cudaMalloc(&c->mk, sizeof(double) * (total + 1)));
+    TB_CUDA(cudaMemcpy(c->mk, h.data(), sizeof(double) * (total + 1), cudaMemcpyHostToDevice));
+    c->mk_len = total + 1;
+  }
+  S.mk = c->mk;
   TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
   int warps = 0;
   TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
