@@ -43,6 +43,7 @@ extern "C" {
 #define TB_STATUS_NUMERICAL_FAILURE 3
 
 typedef struct tb_ctx tb_ctx;
+typedef struct tb_tiled tb_tiled;
 
 /* SolverConfig (solver.py:35-97); lambda_reg/seed are per pixel arrays, theta pinned. */
 typedef struct tb_solver_config {
@@ -100,6 +101,26 @@ int tb_solve(tb_ctx* ctx, int32_t solver, const tb_solver_config* cfg, const voi
              const float* lambda_dev, const uint64_t* seeds_dev, int64_t num_pixels, void* x_dev,
              double* f_final_dev, double* history_dev, int64_t hist_stride,
              int32_t* iterations_dev, int32_t* status_dev, void* stream);
+
+/* Large-dictionary solver driven one round at a time (used by tb_solve automatically when the
+ * warp-per-pixel plan does not fit, and directly by the column-sharded multi-GPU driver).
+ * A round advances every unfinished pixel by one backtracking trial of its current iteration
+ * (solver.py:281-333 / 354-371).  round_a = block draw + r_y, fused adjoint/prox/forward pass over
+ * the local dictionary columns, split reduction into red_dev; the caller may all-reduce red_dev
+ * (sum over column shards) before round_b = test/accept/history/stop.
+ *  red_dev: caller-owned device buffer of P*(2n+4) doubles ([P][n] complex128 forward product
+ *  followed by [P][4] scalars), or NULL for an internal one.  State lives in HBM (3 fp64 copies
+ *  of x per pixel). */
+int tb_tiled_create(tb_ctx* ctx, int32_t solver, const tb_solver_config* cfg, const void* pixels_dev,
+                    const float* lambda_dev, const uint64_t* seeds_dev, int64_t num_pixels,
+                    double* history_dev, int64_t hist_stride, void* red_dev, void* stream,
+                    tb_tiled** out);
+int tb_tiled_round_a(tb_tiled* h, void* stream);
+int tb_tiled_round_b(tb_tiled* h, void* stream);
+int tb_tiled_remaining(tb_tiled* h, int64_t* remaining_host, void* stream);
+int tb_tiled_finish(tb_tiled* h, void* x_dev, double* f_final_dev, int32_t* iterations_dev,
+                    int32_t* status_dev, void* stream);
+int tb_tiled_destroy(tb_tiled* h);
 
 /* SL1MMER stages 2-3 (slimmer.py:77-190): detect_support -> model_select (BIC over fp64 LS
  * refits, rank filter) -> estimate_params (debiased LS amplitudes, grid decode).

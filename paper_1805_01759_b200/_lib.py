@@ -47,6 +47,12 @@ SIGNATURES = {
     "tb_default_lambda": (c_int32, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p]),
     "tb_derive_seeds": (c_int32, [c_uint64, c_int64, c_int64, c_void_p, c_void_p]),
     "tb_solve": (c_int32, [c_void_p, c_int32, ctypes.POINTER(SolverConfigC), c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "tb_tiled_create": (c_int32, [c_void_p, c_int32, ctypes.POINTER(SolverConfigC), c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),
+    "tb_tiled_round_a": (c_int32, [c_void_p, c_void_p]),
+    "tb_tiled_round_b": (c_int32, [c_void_p, c_void_p]),
+    "tb_tiled_remaining": (c_int32, [c_void_p, ctypes.POINTER(c_int64), c_void_p]),
+    "tb_tiled_finish": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tb_tiled_destroy": (c_int32, [c_void_p]),
     "tb_select": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32, ctypes.POINTER(c_int32), c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 

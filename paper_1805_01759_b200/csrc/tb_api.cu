@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "setup.h"
 #include "solver_params.h"
+#include "tiled.h"
 
 struct tb_ctx {
   int device = 0;
@@ -27,6 +28,17 @@ struct tb_ctx {
   unsigned long long* queue = nullptr;
   double* mk = nullptr;  // momentum table (k-2)/(k+1), k = 0..mk_len-1
   int mk_len = 0;
+  std::vector<double> lip_host;  // per-block Lipschitz (host copy)
+  std::vector<int> bstart_host;  // J+1
+};
+
+struct tb_tiled {
+  tb_ctx* ctx = nullptr;
+  tb::TiledParams T{};
+  void* owned = nullptr;  // single device allocation holding every internal buffer
+  bool own_red = false;
+  int max_width = 0;
+  long long rounds = 0;
 };
 
 static thread_local std::string g_err;
@@ -226,6 +238,8 @@ int tb_set_partition(tb_ctx* c, int32_t J, const int64_t* starts, const int64_t*
   c->num_blocks = J;
   c->max_block_width = maxw;
   c->has_partition = true;
+  c->lip_host.assign(lip, lip + J);
+  c->bstart_host = bs;
   return TB_OK;
 }
 
@@ -251,13 +265,10 @@ int tb_derive_seeds(uint64_t run_seed, int64_t first, int64_t P, uint64_t* seeds
   return TB_OK;
 }
 
-int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const float* lam,
-             const uint64_t* seeds, int64_t P, void* x, double* f_final, double* hist, int64_t hist_stride,
-             int32_t* iters, int32_t* status, void* stream) {
+static int check_solve_args(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const uint64_t* seeds, int64_t P,
+                            const double* hist, int64_t hist_stride) {
   if (!c || !cfg) return fail(TB_ERR_INVALID, "null argument");
   if (P < 0) return fail(TB_ERR_INVALID, "num_pixels must be >= 0");
-  if (P == 0) return TB_OK;
-  if (!pixels || !lam || !x || !f_final || !iters || !status) return fail(TB_ERR_INVALID, "null buffer");
   if (solver != TB_SOLVER_RBPG && solver != TB_SOLVER_FISTA && solver != TB_SOLVER_ISTA) return fail(TB_ERR_INVALID, "unknown solver %d", solver);
   if (cfg->max_iters < 1) return fail(TB_ERR_INVALID, "max_iters must be >= 1, got %d", cfg->max_iters);
   if (!(cfg->tol > 0.0)) return fail(TB_ERR_INVALID, "tol must be > 0");
@@ -266,23 +277,292 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   if (cfg->backtrack_cap < 0) return fail(TB_ERR_INVALID, "backtrack_cap must be >= 0");
   const int total = cfg->fixed_iters > 0 ? cfg->fixed_iters : cfg->max_iters;
   if (hist && hist_stride < total + 1) return fail(TB_ERR_INVALID, "hist_stride %lld < iterations + 1", (long long)hist_stride);
+  if (solver == TB_SOLVER_RBPG) {
+    if (!c->has_partition) return fail(TB_ERR_INVALID, "RBPG needs tb_set_partition first");
+    if (cfg->num_blocks != c->num_blocks) return fail(TB_ERR_INVALID, "config num_blocks %d != partition %d", cfg->num_blocks, c->num_blocks);
+    if (!seeds && P > 0) return fail(TB_ERR_INVALID, "RBPG needs per-pixel seeds");
+  } else if (!c->has_lip) {
+    return fail(TB_ERR_INVALID, "ISTA/FISTA need tb_set_lipschitz first");
+  }
+  return TB_OK;
+}
+
+static int ensure_mk(tb_ctx* c, int total, cudaStream_t st) {
+  if (c->mk_len >= total + 1) return TB_OK;
+  // theta_k = 2/(k+1) collapsed to m_k = (k-2)/(k+1) (solver.py:222-224), IEEE double division
+  std::vector<double> h(total + 1);
+  for (int k = 0; k <= total; ++k) h[k] = (k - 2.0) / (k + 1.0);
+  TB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(c->mk);
+  c->mk = nullptr;
+  TB_CUDA(cudaMalloc(&c->mk, sizeof(double) * (total + 1)));
+  TB_CUDA(cudaMemcpy(c->mk, h.data(), sizeof(double) * (total + 1), cudaMemcpyHostToDevice));
+  c->mk_len = total + 1;
+  return TB_OK;
+}
+
+// Does the warp-per-pixel kernel's shared-memory plan fit this problem?
+static bool warp_path_fits(tb_ctx* c, int32_t solver) {
+  const int width = solver == TB_SOLVER_RBPG ? c->max_block_width : (int)c->m;
+  if ((width + 31) / 32 > 16) return false;
+  const int J = solver == TB_SOLVER_RBPG ? c->num_blocks : 1;
+  const size_t slot = tb::warp_slot_bytes((int)c->n, (int)c->m, width, J);
+  return tb::block_table_bytes(J) + 4 * slot <= 227 * 1024;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const float* lam,
+                    const uint64_t* seeds, int64_t P, double* hist, int64_t hist_stride, void* red_dev,
+                    void* stream, tb_tiled** out) {
+  int rc = check_solve_args(c, solver, cfg, seeds, P, hist, hist_stride);
+  if (rc != TB_OK) return rc;
+  if (!out || P < 1 || !pixels || !lam) return fail(TB_ERR_INVALID, "tiled solver needs >= 1 pixel and buffers");
+  cudaStream_t st = (cudaStream_t)stream;
+  TB_CUDA(cudaSetDevice(c->device));
+  const int total = cfg->fixed_iters > 0 ? cfg->fixed_iters : cfg->max_iters;
+  rc = ensure_mk(c, total, st);
+  if (rc != TB_OK) return rc;
+  const bool rb = solver == TB_SOLVER_RBPG;
+  const int J = rb ? c->num_blocks : 1;
+  const int n = (int)c->n;
+  const long long m = c->m;
+  const int maxw = rb ? c->max_block_width : (int)m;
+  // split width: enough CTAs for ~4 waves of 2 CTAs/SM, at least one column tile
+  const long long tiles = (P + tb::TL_PT - 1) / tb::TL_PT + (rb ? J : 0);
+  long long s_target = (4ll * 2 * c->num_sms + tiles - 1) / tiles;
+  if (s_target < 1) s_target = 1;
+  long long sw = (maxw + s_target - 1) / s_target;
+  sw = ((sw + tb::TL_CT - 1) / tb::TL_CT) * tb::TL_CT;
+  if (sw < tb::TL_CT) sw = tb::TL_CT;
+  const int max_splits = (int)((maxw + sw - 1) / sw);
+
+  // one allocation for all internal state
+  size_t sz[32];
+  int ns = 0;
+  sz[ns++] = align256(sizeof(double2) * 3ull * P * m);   // X3
+  sz[ns++] = align256(sizeof(int) * P * 6);              // phase k trial status blk perm
+  sz[ns++] = align256(sizeof(int) * P * 3);              // roles
+  sz[ns++] = align256(sizeof(double) * P * 3);           // F l1 alpha
+  sz[ns++] = align256(sizeof(double) * P * 16);          // ring
+  sz[ns++] = align256(sizeof(double) * P * J);           // l1blk
+  sz[ns++] = align256(sizeof(double2) * P * n * 3);      // r axp ry
+  sz[ns++] = align256(sizeof(double2) * P * (rb ? J : 1) * n);  // delta
+  sz[ns++] = align256(sizeof(float2) * P * n);           // ry32
+  sz[ns++] = align256(sizeof(int4) * (tiles + J + 1));    // tiles
+  sz[ns++] = align256(sizeof(int) * 2);                  // ntiles remaining
+  sz[ns++] = align256(sizeof(double2) * (size_t)max_splits * P * n);  // part
+  sz[ns++] = align256(sizeof(double) * (size_t)max_splits * P * 4);   // psc
+  sz[ns++] = red_dev ? 0 : align256(sizeof(double) * P * (2 * n + 4));  // red + redsc
+  sz[ns++] = align256(sizeof(double) * J * 2);           // alpha0, cdf
+  sz[ns++] = align256(sizeof(int) * (J + 1));            // bstart
+  size_t tot = 0;
+  for (int i = 0; i < ns; ++i) tot += sz[i];
+  size_t fr = 0, tt = 0;
+  cudaMemGetInfo(&fr, &tt);
+  if (tot > fr) return fail(TB_ERR_CAPACITY, "tiled solver needs %.1f GB for %lld pixels, %.1f GB free", tot / 1e9, (long long)P, fr / 1e9);
+  unsigned char* base = nullptr;
+  TB_CUDA(cudaMallocAsync((void**)&base, tot, st));
+  tb_tiled* h = new tb_tiled();
+  h->ctx = c;
+  h->owned = base;
+  h->own_red = red_dev == nullptr;
+  h->max_width = maxw;
+  tb::TiledParams& T = h->T;
+  unsigned char* q = base;
+  int k = 0;
+  auto take = [&](size_t) { unsigned char* r = q; q += sz[k++]; return r; };
+  T.X3 = (double2*)take(0);
+  int* ints = (int*)take(0);
+  T.phase = ints;
+  T.k = ints + P;
+  T.trial = ints + 2 * P;
+  T.status = ints + 3 * P;
+  T.blk = ints + 4 * P;
+  T.perm = ints + 5 * P;
+  T.roles = (int*)take(0);
+  double* dbl = (double*)take(0);
+  T.F = dbl;
+  T.l1 = dbl + P;
+  T.alpha = dbl + 2 * P;
+  T.ring = (double*)take(0);
+  T.l1blk = (double*)take(0);
+  double2* vec = (double2*)take(0);
+  T.r = vec;
+  T.axp = vec + (size_t)P * n;
+  T.ry = vec + 2 * (size_t)P * n;
+  T.delta = (double2*)take(0);
+  T.ry32 = (float2*)take(0);
+  T.tiles = (int4*)take(0);
+  int* cnts = (int*)take(0);
+  T.ntiles = cnts;
+  T.remaining = cnts + 1;
+  T.part = (double2*)take(0);
+  T.psc = (double*)take(0);
+  double* redp = red_dev ? (double*)red_dev : (double*)take(0);
+  if (red_dev) k++;
+  T.red = (double2*)redp;
+  T.redsc = redp + 2 * (size_t)P * n;
+  double* tabs = (double*)take(0);
+  int* bst = (int*)take(0);
+  T.alpha0 = tabs;
+  T.cdf = tabs + J;
+  T.bstart = bst;
+  // block tables: alpha0 = scale / max(L, 1e-300) (solver.py:295, 345), cdf, starts
+  std::vector<double> ht(2 * J);
+  std::vector<int> hb(J + 1);
+  std::vector<double> cdf(J);
+  if (rb) {
+    TB_CUDA(cudaMemcpy(cdf.data(), c->cdf, sizeof(double) * J, cudaMemcpyDeviceToHost));
+    for (int j = 0; j < J; ++j) ht[j] = cfg->alpha_init_scale / fmax(c->lip_host[j], 1e-300);
+    for (int j = 0; j <= J; ++j) hb[j] = c->bstart_host[j];
+  } else {
+    ht[0] = cfg->alpha_init_scale / fmax(c->lip_full, 1e-300);
+    cdf[0] = 1.0;
+    hb[0] = 0;
+    hb[1] = (int)m;
+  }
+  for (int j = 0; j < J; ++j) ht[J + j] = cdf[j];
+  TB_CUDA(cudaMemcpyAsync(tabs, ht.data(), sizeof(double) * 2 * J, cudaMemcpyHostToDevice, st));
+  TB_CUDA(cudaMemcpyAsync(bst, hb.data(), sizeof(int) * (J + 1), cudaMemcpyHostToDevice, st));
+  T.A = c->A;
+  T.n = n;
+  T.m = (int)m;
+  T.mode = solver;
+  T.J = J;
+  T.mk = c->mk;
+  T.total_iters = total;
+  T.fixed = cfg->fixed_iters > 0;
+  T.cap = cfg->backtrack_cap;
+  T.tol = cfg->tol;
+  T.c_alpha = cfg->c_alpha;
+  T.split_width = (int)sw;
+  T.max_splits = max_splits;
+  T.P = (int)P;
+  T.B = (const float2*)pixels;
+  T.lam = lam;
+  T.seeds = seeds;
+  T.hist = hist;
+  T.hist_stride = hist_stride;
+  // x = prev = 0 (solver.py:270-272, 348)
+  TB_CUDA(cudaMemsetAsync(T.X3, 0, sizeof(double2) * 2ull * P * m, st));
+  const int rem = (int)P;
+  TB_CUDA(cudaMemcpyAsync(T.remaining, &rem, sizeof(int), cudaMemcpyHostToDevice, st));
+  TB_CUDA(tb::tiled_init(T, st));
+  TB_CUDA(cudaStreamSynchronize(st));
+  *out = h;
+  return TB_OK;
+}
+
+int tb_tiled_round_a(tb_tiled* h, void* stream) {
+  if (!h) return fail(TB_ERR_INVALID, "null handle");
+  cudaStream_t st = (cudaStream_t)stream;
+  TB_CUDA(cudaSetDevice(h->ctx->device));
+  TB_CUDA(tb::tiled_prep(h->T, st));
+  TB_CUDA(tb::tiled_pass(h->T, h->ctx->num_sms, st));
+  TB_CUDA(tb::tiled_reduce(h->T, st));
+  return TB_OK;
+}
+
+int tb_tiled_round_b(tb_tiled* h, void* stream) {
+  if (!h) return fail(TB_ERR_INVALID, "null handle");
+  TB_CUDA(cudaSetDevice(h->ctx->device));
+  TB_CUDA(tb::tiled_update(h->T, (cudaStream_t)stream));
+  h->rounds++;
+  return TB_OK;
+}
+
+int tb_tiled_remaining(tb_tiled* h, int64_t* out, void* stream) {
+  if (!h || !out) return fail(TB_ERR_INVALID, "null argument");
+  int v = 0;
+  TB_CUDA(cudaMemcpyAsync(&v, h->T.remaining, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  TB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  *out = v;
+  return TB_OK;
+}
+
+int tb_tiled_finish(tb_tiled* h, void* x, double* f_final, int32_t* iters, int32_t* status, void* stream) {
+  if (!h || !x || !f_final || !iters || !status) return fail(TB_ERR_INVALID, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  TB_CUDA(cudaSetDevice(h->ctx->device));
+  h->T.X = (float2*)x;
+  h->T.f_final = f_final;
+  h->T.iters = iters;
+  TB_CUDA(tb::tiled_finish(h->T, st));
+  TB_CUDA(cudaMemcpyAsync(status, h->T.status, sizeof(int) * h->T.P, cudaMemcpyDeviceToDevice, st));
+  return TB_OK;
+}
+
+int tb_tiled_destroy(tb_tiled* h) {
+  if (!h) return TB_OK;
+  cudaSetDevice(h->ctx->device);
+  cudaDeviceSynchronize();
+  cudaFree(h->owned);
+  delete h;
+  return TB_OK;
+}
+
+static int solve_tiled(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const float* lam,
+                       const uint64_t* seeds, int64_t P, void* x, double* f_final, double* hist, int64_t hist_stride,
+                       int32_t* iters, int32_t* status, cudaStream_t st) {
+  // pixel chunks sized to the free HBM (state is 3 fp64 copies of x per pixel)
+  size_t fr = 0, tt = 0;
+  TB_CUDA(cudaMemGetInfo(&fr, &tt));
+  const double per_px = 3.0 * 16.0 * (double)c->m + 64.0 * c->n * (solver == TB_SOLVER_RBPG ? c->num_blocks + 4 : 5) + 4096;
+  long long chunk = (long long)(0.6 * (double)fr / per_px);
+  if (chunk < 1) return fail(TB_ERR_CAPACITY, "not enough device memory for one pixel of m = %lld", (long long)c->m);
+  if (chunk > 8192) chunk = 8192;
+  const int total = cfg->fixed_iters > 0 ? cfg->fixed_iters : cfg->max_iters;
+  for (long long p0 = 0; p0 < P; p0 += chunk) {
+    const long long pc = P - p0 < chunk ? P - p0 : chunk;
+    tb_tiled* h = nullptr;
+    int rc = tb_tiled_create(c, solver, cfg, (const float2*)pixels + p0 * c->n, lam + p0, seeds ? seeds + p0 : nullptr, pc,
+                             hist ? hist + p0 * hist_stride : nullptr, hist_stride, nullptr, st, &h);
+    if (rc != TB_OK) return rc;
+    const long long max_rounds = (long long)total * (cfg->backtrack_cap + 1) + 1;
+    for (long long r = 0; r < max_rounds; ++r) {
+      rc = tb_tiled_round_a(h, st);
+      if (rc == TB_OK) rc = tb_tiled_round_b(h, st);
+      if (rc != TB_OK) {
+        tb_tiled_destroy(h);
+        return rc;
+      }
+      if ((r + 1) % 16 == 0 || r + 1 >= total) {
+        int64_t rem = 0;
+        rc = tb_tiled_remaining(h, &rem, st);
+        if (rc != TB_OK || rem == 0) break;
+      }
+    }
+    rc = tb_tiled_finish(h, (float2*)x + p0 * c->m, f_final + p0, iters + p0, status + p0, st);
+    TB_CUDA(cudaStreamSynchronize(st));
+    tb_tiled_destroy(h);
+    if (rc != TB_OK) return rc;
+  }
+  return TB_OK;
+}
+
+int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const float* lam,
+             const uint64_t* seeds, int64_t P, void* x, double* f_final, double* hist, int64_t hist_stride,
+             int32_t* iters, int32_t* status, void* stream) {
+  int rc = check_solve_args(c, solver, cfg, seeds, P, hist, hist_stride);
+  if (rc != TB_OK) return rc;
+  if (P == 0) return TB_OK;
+  if (!pixels || !lam || !x || !f_final || !iters || !status) return fail(TB_ERR_INVALID, "null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  TB_CUDA(cudaSetDevice(c->device));
+  const int total = cfg->fixed_iters > 0 ? cfg->fixed_iters : cfg->max_iters;
+  rc = ensure_mk(c, total, st);
+  if (rc != TB_OK) return rc;
+  if (!warp_path_fits(c, solver))
+    return solve_tiled(c, solver, cfg, pixels, lam, seeds, P, x, f_final, hist, hist_stride, iters, status, st);
   tb::SolveParams S{};
   S.A = c->A;
   S.n = (int)c->n;
   S.m = (int)c->m;
   S.ms = (int)(c->m | 1);
   S.mode = solver;
-  if (solver == TB_SOLVER_RBPG) {
-    if (!c->has_partition) return fail(TB_ERR_INVALID, "RBPG needs tb_set_partition first");
-    if (cfg->num_blocks != c->num_blocks) return fail(TB_ERR_INVALID, "config num_blocks %d != partition %d", cfg->num_blocks, c->num_blocks);
-    if (!seeds) return fail(TB_ERR_INVALID, "RBPG needs per-pixel seeds");
-    S.max_width = c->max_block_width;
-  } else {
-    if (!c->has_lip) return fail(TB_ERR_INVALID, "ISTA/FISTA need tb_set_lipschitz first");
-    S.max_width = (int)c->m;
-  }
-  if ((S.max_width + 31) / 32 > 16) return fail(TB_ERR_CAPACITY, "active width %d exceeds the warp solver's 512 columns", S.max_width);
-  S.num_blocks = c->num_blocks;
+  S.max_width = solver == TB_SOLVER_RBPG ? c->max_block_width : (int)c->m;
+  S.num_blocks = solver == TB_SOLVER_RBPG ? c->num_blocks : 1;
   S.blk_start = c->blk_start;
   S.blk_lip = c->blk_lip;
   S.cdf = c->cdf;
@@ -304,19 +584,6 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   S.iters = iters;
   S.status = status;
   S.queue = c->queue;
-  cudaStream_t st = (cudaStream_t)stream;
-  TB_CUDA(cudaSetDevice(c->device));
-  if (c->mk_len < total + 1) {
-    // theta_k = 2/(k+1) collapsed to m_k = (k-2)/(k+1) (solver.py:222-224), IEEE double division
-    std::vector<double> h(total + 1);
-    for (int k = 0; k <= total; ++k) h[k] = (k - 2.0) / (k + 1.0);
-    TB_CUDA(cudaStreamSynchronize(st));
-    cudaFree(c->mk);
-    c->mk = nullptr;
-    TB_CUDA(cudaMalloc(&c->mk, sizeof(double) * (total + 1)));
-    TB_CUDA(cudaMemcpy(c->mk, h.data(), sizeof(double) * (total + 1), cudaMemcpyHostToDevice));
-    c->mk_len = total + 1;
-  }
   S.mk = c->mk;
   TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
   int warps = 0;

@@ -335,8 +335,14 @@ class Dictionary:
             _lib.check(self._lib.tb_derive_seeds(int(run_seed) & (2**64 - 1), int(first_pixel_id), int(num_pixels), _lib.ptr(seeds), self._stream()))
         return seeds
 
-    def solve(self, pixels, lam, config: SolverConfig, backend: str = "rbpg", seeds=None, history: bool = False, out=None) -> BatchSolution:
-        """Solve every pixel of a stack with one persistent kernel launch."""
+    def solve(self, pixels, lam, config: SolverConfig, backend: str = "rbpg", seeds=None, history: bool = False, out=None, path: str = "auto", allreduce=None) -> BatchSolution:
+        """Solve every pixel of a stack on the device.
+
+        ``path`` "auto" lets the library pick the warp-per-pixel kernel (dictionary and iterate in
+        shared memory) or the tiled large-dictionary solver; "tiled" forces the latter, driven
+        round by round from here so that ``allreduce(red)`` (sum over column shards, e.g.
+        torch.distributed.all_reduce) can run between the pass and the update.
+        """
         torch = _torch()
         if backend not in _lib.SOLVER_CODES:
             raise ConfigurationError(f"unknown iterative backend {backend!r}")
@@ -375,6 +381,11 @@ class Dictionary:
         hist = torch.full((p, total + 1), float("nan"), dtype=torch.float64, device=self.device) if history else None
         cfg = config.to_c()
         t0 = time.perf_counter()
+        if path == "tiled" or allreduce is not None:
+            self._solve_tiled(backend, cfg, b, lam_t, seeds_t, p, x, ffin, hist, total, its, st, allreduce)
+            res = BatchSolution(x_hat=x, objective_final=ffin, iterations=its, status=st, history=hist, wall_time=time.perf_counter() - t0)
+            res._no_append = backend != "rbpg"
+            return res
         with torch.cuda.device(self.device):
             _lib.check(
                 self._lib.tb_solve(
@@ -385,6 +396,38 @@ class Dictionary:
         res = BatchSolution(x_hat=x, objective_final=ffin, iterations=its, status=st, history=hist, wall_time=time.perf_counter() - t0)
         res._no_append = backend != "rbpg"
         return res
+
+
+    def _solve_tiled(self, backend, cfg, b, lam_t, seeds_t, p, x, ffin, hist, total, its, st, allreduce):
+        torch = _torch()
+        if p == 0:
+            return
+        red = torch.zeros(p * (2 * self.n + 4), dtype=torch.float64, device=self.device)
+        h = ctypes.c_void_p()
+        stream = self._stream()
+        with torch.cuda.device(self.device):
+            _lib.check(
+                self._lib.tb_tiled_create(
+                    self._h, _lib.SOLVER_CODES[backend], ctypes.byref(cfg), _lib.ptr(b), _lib.ptr(lam_t), _lib.ptr(seeds_t), p,
+                    _lib.ptr(hist), total + 1 if hist is not None else 0, _lib.ptr(red), stream, ctypes.byref(h),
+                )
+            )
+            try:
+                rem = ctypes.c_int64()
+                max_rounds = total * (cfg.backtrack_cap + 1) + 1
+                for r in range(max_rounds):
+                    _lib.check(self._lib.tb_tiled_round_a(h, stream))
+                    if allreduce is not None:
+                        allreduce(red)
+                    _lib.check(self._lib.tb_tiled_round_b(h, stream))
+                    if (r + 1) % 16 == 0 or r + 1 >= total:
+                        _lib.check(self._lib.tb_tiled_remaining(h, ctypes.byref(rem), stream))
+                        if rem.value == 0:
+                            break
+                _lib.check(self._lib.tb_tiled_finish(h, _lib.ptr(x), _lib.ptr(ffin), _lib.ptr(its), _lib.ptr(st), stream))
+                torch.cuda.synchronize(self.device)
+            finally:
+                self._lib.tb_tiled_destroy(h)
 
 
 _CACHE: "OrderedDict[tuple, Dictionary]" = OrderedDict()
