@@ -275,7 +275,7 @@ def run_b200(args):
             "clocks": clk,
             "solver_stats": {"mean_iterations": float(its.mean()), "converged_frac": float((st == 0).mean()), "max_iters_frac": float((st == 1).mean())},
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             from oracle import tomo_oracle as O
             from paper_1805_01759_b200.synth import lambda_from_beta
 

@@ -348,13 +348,15 @@ class Dictionary:
             raise ConfigurationError(f"unknown iterative backend {backend!r}")
         b = self._pixels(pixels)
         p = int(b.shape[0])
+        if not isinstance(lam, torch.Tensor):
+            lam_h = np.asarray(lam, dtype=np.float64).reshape(-1)
+            if not (np.all(np.isfinite(lam_h)) and np.all(lam_h >= 0)):
+                raise ConfigurationError("lambda_reg must be finite and >= 0")  # prox.py:47-48
         lam_t = torch.as_tensor(lam, dtype=torch.float32).reshape(-1).to(self.device)
         if lam_t.numel() == 1 and p != 1:
             lam_t = lam_t.expand(p).contiguous()
         if lam_t.numel() != p:
             raise ConfigurationError(f"need one lambda per pixel ({p}), got {lam_t.numel()}")
-        if not bool(torch.isfinite(lam_t).all()) or bool((lam_t < 0).any()):
-            raise ConfigurationError("lambda_reg must be finite and >= 0")
         seeds_t = None
         if backend == "rbpg":
             self.partition(config.num_blocks)
