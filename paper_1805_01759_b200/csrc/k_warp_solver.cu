@@ -57,6 +57,9 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(cons
   __syncthreads();
   off += block_table_bytes(J);
   const double alpha0_full = P.alpha_scale / fmax(P.lip_full, 1e-300);  // solver.py:345
+  double cdf_r[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) cdf_r[q] = (RB && q < J) ? s_cdf[q] : 2.0;
   const size_t per_warp = warp_slot_bytes(n, m, P.max_width, J);
   unsigned char* wb = smem + off + (size_t)warp * per_warp;
   double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA)
@@ -145,7 +148,13 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(cons
       if (RB) {
         double u = raw_to_unit(philox_next(rng));
         int j = 0;
-        while (j < J - 1 && s_cdf[j] <= u) ++j;
+        if (J <= 8) {
+          // searchsorted(cdf, u, 'right') with cdf[J-1] == 1 > u: count of cdf[j] <= u, j < J-1
+#pragma unroll
+          for (int q = 0; q < 7; ++q) j += (q < J - 1 && cdf_r[q] <= u) ? 1 : 0;
+        } else {
+          while (j < J - 1 && s_cdf[j] <= u) ++j;
+        }
         blk = j;
         cs = s_bstart[blk];
         ce = s_bstart[blk + 1];

@@ -49,6 +49,15 @@ __host__ __device__ inline size_t block_table_bytes(int J) {
   return (b + 15) & ~(size_t)15;
 }
 
+// RBPG group-kernel slot: fp64 r, fp64 x, fp64 broadcast [width], fp32 d = x - prev, fp32 r_y,
+// 16-double ring, J-double per-block l1 cache
+__host__ __device__ inline size_t rbpg_slot_bytes(int n, int m, int width, int J) {
+  size_t b = (size_t)n * 16 + (size_t)m * 16 + (size_t)width * 16 + (size_t)m * 8 + (size_t)(n + (n & 1)) * 8 + 16 * 8 + (size_t)J * 8;
+  return (b + 15) & ~(size_t)15;
+}
+
 cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps);
+bool rbpg_group_supported(int n, int max_width);
+cudaError_t launch_rbpg_group(const SolveParams& P, int num_sms, cudaStream_t st);
 
 }  // namespace tb

@@ -1,6 +1,7 @@
 // C ABI implementation (include/tomobpdn_b200.h): context management, validation, launches.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -586,8 +587,15 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   S.queue = c->queue;
   S.mk = c->mk;
   TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
-  int warps = 0;
-  TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
+  const char* force = getenv("TB_RBPG_KERNEL");
+  // the half-warp-per-pixel RBPG variant measured slower on cfg2 (0.68 vs 1.07 M px/s); opt-in only
+  const bool use_group = solver == TB_SOLVER_RBPG && tb::rbpg_group_supported(S.n, S.max_width) && force && strcmp(force, "group") == 0;
+  if (use_group) {
+    TB_CUDA(tb::launch_rbpg_group(S, c->num_sms, st));
+  } else {
+    int warps = 0;
+    TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
+  }
   return TB_OK;
 }
 
