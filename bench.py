@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--pixels", type=int, default=None)
     ap.add_argument("--cpu-sample", type=int, default=None, help="pixels per CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", default="auto", choices=["auto", "tiled"], help="solver kernel family (auto = library choice)")
     return ap.parse_args()
 
 
@@ -196,7 +197,7 @@ def run_b200(args):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        sol = d.solve(pix_dev, lam, scfg, args.backend, seeds=seeds)
+        sol = d.solve(pix_dev, lam, scfg, args.backend, seeds=seeds, path=args.path)
         b.record(stream)
         est = tb.select_batch(d, sol.x_hat, pix_dev, grid, batch.k_max)
         ks.append(a)

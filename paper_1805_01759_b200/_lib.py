@@ -13,7 +13,7 @@ import os
 from .exceptions import CapacityError, ConfigurationError, NumericalError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtomobpdn_b200.so")
+LIB_PATH = os.environ.get("TB_LIB_PATH") or os.path.join(HERE, "lib", "libtomobpdn_b200.so")
 
 TB_OK, TB_ERR_INVALID, TB_ERR_CUDA, TB_ERR_CAPACITY = 0, 1, 2, 3
 SOLVER_CODES = {"rbpg": 0, "fista": 1, "ista": 2}

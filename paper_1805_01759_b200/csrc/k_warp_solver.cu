@@ -23,10 +23,14 @@
 #include "common.cuh"
 #include "solver_params.h"
 
+#ifndef TB_WARP_LB
+#define TB_WARP_LB 448
+#endif
+
 namespace tb {
 
 template <bool RB, int MAXT, int MAXQ, bool ASMEM>
-__global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(const SolveParams P) {
+__global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -65,9 +69,9 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(cons
   double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA)
   double2* apv = rv + n;                         // A x_prev (FISTA)
   double2* xs = apv + n;                         // x (fp64 iterate)
-  double2* ps = xs + m;                          // prev block values (RBPG) / x_prev (FISTA)
-  double2* zs = ps + m;                          // broadcast buffer for forward products [max_width]
-  float2* ryv = reinterpret_cast<float2*>(zs + P.max_width);  // r_y rounded for the adjoint
+  double2* zs = xs + m;                          // broadcast buffer for forward products [max_width]
+  float2* ds = reinterpret_cast<float2*>(zs + P.max_width);  // d = x - prev, fp32 (y = x + m_k d)
+  float2* ryv = ds + m;                          // r_y rounded for the adjoint
   float2* bv = ryv + n;                          // b
   double* ring = reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
   double* l1blk = ring + 16;                     // RBPG: sum |x_b| per block (updated on accept)
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(cons
     // ---- initial state: x = 0, prev = 0, r = -b, F0 = ||b||^2 (solver.py:270-276, 349)
     for (int c = lane; c < m; c += 32) {
       xs[c] = make_double2(0.0, 0.0);
-      ps[c] = make_double2(0.0, 0.0);
+      ds[c] = make_float2(0.f, 0.f);
     }
     double fb = 0.0;
     for (int i = lane; i < n; i += 32) {
@@ -175,11 +179,13 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(cons
         bool nz = false;
         if (cl < width) {
           const double2 xv = xs[cs + cl];
-          const double2 pv = ps[cs + cl];
           double2 yv = xv;
           if (!ista) {
-            yv.x = fma(mk, xv.x - pv.x, xv.x);
-            yv.y = fma(mk, xv.y - pv.y, xv.y);
+            // y = x + m_k (x - prev) with the extrapolation memory kept as d = x - prev in fp32;
+            // d is exactly 0 after a rejected visit, so `np.any(dy)` (solver.py:291) is preserved
+            const float2 dv = ds[cs + cl];
+            yv.x = fma(mk, (double)dv.x, xv.x);
+            yv.y = fma(mk, (double)dv.y, xv.y);
           }
           y[t] = yv;
           if (RB) {
@@ -346,8 +352,13 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(cons
         for (int t = 0; t < MAXT; ++t) {
           const int cl = lane + 32 * t;
           if (cl < width) {
-            ps[cs + cl] = xs[cs + cl];
-            if (accept) xs[cs + cl] = z[RB ? t : 0];
+            if (accept) {
+              const double2 xv = xs[cs + cl], zv = z[RB ? t : 0];
+              ds[cs + cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
+              xs[cs + cl] = zv;
+            } else {
+              ds[cs + cl] = make_float2(0.f, 0.f);  // prev_b <- x_b (solver.py:325)
+            }
           }
         }
         if (accept) {
@@ -366,8 +377,9 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : 384) warp_solver_kernel(cons
         for (int t = 0; t < MAXT; ++t) {
           const int cl = lane + 32 * t;
           if (cl < width) {
-            ps[cl] = xs[cl];
-            xs[cl] = zs[cl];
+            const double2 xv = xs[cl], zv = zs[cl];
+            ds[cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
+            xs[cl] = zv;
           }
         }
 #pragma unroll
@@ -456,7 +468,7 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   const size_t tables = block_table_bytes(J);
   const size_t a_bytes = ((size_t)P.n * P.ms * sizeof(float2) + 15) & ~(size_t)15;
   const size_t cap = 227 * 1024;
-  const int max_warps = maxt >= 8 ? 8 : 12;
+  const int max_warps = maxt >= 8 ? 8 : TB_WARP_LB / 32;
   bool asmem = a_bytes + tables + 4 * slot <= cap;
   size_t avail = cap - tables - (asmem ? a_bytes : 0);
   int warps = (int)(avail / slot);
