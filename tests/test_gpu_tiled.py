@@ -144,3 +144,62 @@ def test_cfg5_power_iteration_and_rbpg_rhs(tb):
     rx = np.array([r["x_hat"] for r in ref])
     err = np.linalg.norm(bs.x_hat.cpu().numpy() - rx, axis=1) / np.linalg.norm(rx, axis=1)
     assert err.max() <= 1e-4
+
+
+@pytest.mark.parametrize("backend", ["rbpg", "fista", "ista"])
+def test_tiled_solver_edges(tb, golden, backend):
+    """Closed form, zero measurement, fixed_iters, alpha_init_scale=4 and line-search failure on the
+    tiled path, against the reference golden vectors (test_solver.py:185-247)."""
+
+    def solve(a, b, lam, cfg):
+        d = tb.Dictionary(np.asarray(a))
+        seeds = np.array([int(cfg.seed)], dtype=np.uint64)
+        return d.solve(np.asarray(b).reshape(1, -1), np.array([lam]), cfg, backend, seeds=seeds, history=True, path="tiled").solution(0)
+
+    sol = solve(np.eye(6), golden["edge/eye_b"], 0.5, tb.SolverConfig(num_blocks=2, max_iters=2000, tol=1e-12))
+    np.testing.assert_allclose(sol.x_hat, golden[f"edge/eye_{backend}_x"], atol=2e-6)
+    sol = solve(np.eye(4), np.zeros(4), 0.5, tb.SolverConfig(num_blocks=2, max_iters=50))
+    assert tb.solver.STATUS_BY_CODE.index(sol.status) == int(golden[f"edge/zero_{backend}_status"])
+    np.testing.assert_array_equal(sol.objective_history, golden[f"edge/zero_{backend}_hist"])
+    if backend == "ista":
+        return
+    a, b, lam = golden["cfg1/a"], golden["cfg1/b"][3], float(golden["cfg1/lam"][3])
+    sol = solve(a, b, lam, tb.SolverConfig(num_blocks=8, fixed_iters=37, tol=1e-1, seed=9))
+    assert sol.iterations_used == 37
+    np.testing.assert_allclose(sol.objective_history, golden[f"edge/fixed_{backend}_hist"], rtol=1e-5)
+    sol = solve(a, b, lam, tb.SolverConfig(num_blocks=8, max_iters=60, tol=1e-6, alpha_init_scale=4.0, seed=9))
+    ref = golden[f"edge/scale4_{backend}_hist"]
+    assert sol.objective_history.size == ref.size
+    np.testing.assert_allclose(sol.objective_history, ref, rtol=1e-4)
+    sol = solve(a, b, lam, tb.SolverConfig(num_blocks=8, max_iters=60, tol=1e-6, alpha_init_scale=1e30, c_alpha=0.999999, seed=9))
+    assert sol.status == tb.SolverStatus.LINE_SEARCH_FAILURE
+    assert sol.iterations_used == int(golden[f"edge/lsfail_{backend}_iters"])
+    np.testing.assert_allclose(sol.objective_history, golden[f"edge/lsfail_{backend}_hist"], rtol=1e-6)
+
+
+def test_cfg5_selection_kmax3_vs_oracle(tb):
+    """k_max = 3 on the 256 x 64 x 64 motion grid: joint argmax decode and BIC with p = 5."""
+    from paper_1805_01759_b200.synth import make_config
+
+    c5 = make_config(5, num_pixels=3)
+    d = tb.Dictionary(c5.dictionary)
+    rng = np.random.default_rng(1)
+    m = c5.m
+    x = np.zeros((3, m), np.complex64)
+    for p in range(3):  # sparse profiles with a few peaks, plus the true support
+        idx = rng.choice(m, 12, replace=False)
+        x[p, idx] = (rng.standard_normal(12) + 1j * rng.standard_normal(12)).astype(np.complex64)
+        x[p, c5.truth_support[p]] = 3.0 + 0.1 * np.arange(len(c5.truth_support[p]))  # no exact ties (numpy argsort order on ties is implementation-defined)
+    est = tb.select_batch(d, torch.from_numpy(x).cuda(), c5.pixels, c5.grid, 3)
+    a = c5.dictionary.astype(np.complex128)
+    for p in range(3):
+        cands = O.detect_support(x[p].astype(np.complex128), c5.grid.shape, 3)
+        k, sup, sc = O.model_select(a, c5.pixels[p].astype(np.complex128), cands, 3, 5)
+        ref = O.estimate_params(a, c5.pixels[p].astype(np.complex128), c5.grid, sup)
+        k_gpu = int(est.model_order[p])
+        assert k_gpu == k
+        assert list(est.support[p, :k].cpu().numpy()) == list(sup)
+        np.testing.assert_allclose(est.amplitudes[p, :k].cpu().numpy(), ref["amplitudes"], rtol=1e-9)
+        np.testing.assert_allclose(est.elevations[p, :k].cpu().numpy(), ref["elevations"])
+        np.testing.assert_allclose(est.motion_params[p, :k].cpu().numpy(), ref["motion_params"])
+        np.testing.assert_allclose(est.selection_scores[p, : k + 1].cpu().numpy()[: len(sc)], sc[: k + 1], rtol=1e-10)
