@@ -122,6 +122,17 @@ int tb_tiled_finish(tb_tiled* h, void* x_dev, double* f_final_dev, int32_t* iter
                     int32_t* status_dev, void* stream);
 int tb_tiled_destroy(tb_tiled* h);
 
+/* build_steering_matrix (model.py:296-323) on the device: out[i, c] = exp(sign j 2 pi phase_i(col0+c))
+ * with phase_i(k) = xi_i s(k) + sum_a eta_{a,i} p_a(k) over the row-major grid (elevation leading);
+ * sign = +1 is the reference convention, -1 the BASELINE.json one.  Writes complex64
+ * [n][ncols] for the column range [col0, col0 + ncols) -- a whole dictionary or one rank's shard.
+ *  xi_dev double [n]; eta_dev double [n_axes][n]; elev_dev double [n_elev];
+ *  motion_dev double axis values concatenated; motion_sizes_host int32 [n_axes]. */
+int tb_build_steering(int device, const double* xi_dev, const double* eta_dev, int64_t n, int32_t n_axes,
+                      const double* elev_dev, int64_t n_elev, const double* motion_dev,
+                      const int32_t* motion_sizes_host, int64_t col0, int64_t ncols, double sign,
+                      void* out_dev, void* stream);
+
 /* SL1MMER stages 2-3 (slimmer.py:77-190): detect_support -> model_select (BIC over fp64 LS
  * refits, rank filter) -> estimate_params (debiased LS amplitudes, grid decode).
  *  grid: n_elev elevation bins x inner motion bins (inner = prod motion sizes, flat index

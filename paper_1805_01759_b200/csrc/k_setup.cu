@@ -310,4 +310,41 @@ cudaError_t power_iter_large(const float2* A, int n, int m, long long start, lon
   return e;
 }
 
+// ------------------------------------------------------------------ steering dictionary
+// build_steering_matrix (model.py:296-323): A[i, k] = exp(sign * j 2 pi phase_i(k)) with
+// phase_i(k) = xi_i s(k) + sum_a eta_{a,i} p_a(k), k row-major over (elevation, motion axes...).
+// The phase is accumulated in the reference's order (outer(xi, s) then += outer(eta_a, p_a)) with
+// explicit round-to-nearest ops (no FMA contraction), then 2 pi * phase, cos/sin in fp64, rounded
+// to complex64.  Columns [col0, col0 + ncols) of the flat grid are produced (a column shard).
+__global__ void steering_kernel(const double* __restrict__ xi, const double* __restrict__ eta, int n, int n_axes,
+                                const double* __restrict__ elev, const double* __restrict__ motion, int ms0, int ms1,
+                                long long col0, long long ncols, double sign, float2* __restrict__ out) {
+  const long long total = (long long)n * ncols;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / ncols);
+    const long long c = idx - (long long)i * ncols;
+    const long long k = col0 + c;
+    const long long inner = (long long)ms0 * ms1;
+    const long long s_idx = k / inner;
+    const long long rem = k - s_idx * inner;
+    double ph = __dmul_rn(xi[i], elev[s_idx]);
+    if (n_axes >= 1) {
+      const long long j0 = n_axes == 2 ? rem / ms1 : rem;
+      ph = __dadd_rn(ph, __dmul_rn(eta[i], motion[j0]));
+      if (n_axes == 2) ph = __dadd_rn(ph, __dmul_rn(eta[n + i], motion[ms0 + (rem % ms1)]));
+    }
+    const double arg = __dmul_rn(sign * 6.283185307179586, ph);
+    double sv, cv;
+    sincos(arg, &sv, &cv);
+    out[(size_t)i * ncols + c] = make_float2((float)cv, (float)sv);
+  }
+}
+
+cudaError_t launch_steering(const double* xi, const double* eta, int n, int n_axes, const double* elev, const double* motion,
+                            int ms0, int ms1, long long col0, long long ncols, double sign, float2* out, int num_sms, cudaStream_t st) {
+  if (n <= 0 || ncols <= 0) return cudaSuccess;
+  steering_kernel<<<num_sms * 8, 256, 0, st>>>(xi, eta, n, n_axes, elev, motion, ms0, ms1, col0, ncols, sign, out);
+  return cudaGetLastError();
+}
+
 }  // namespace tb

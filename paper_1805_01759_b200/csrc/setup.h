@@ -16,6 +16,9 @@ cudaError_t launch_power_small(const float2* A, int n, int m, const long long* s
 cudaError_t power_iter_large(const float2* A, int n, int m, long long start, long long stop, double2* v,
                              double2* u, int max_iter, double rtol, double* result, int num_sms, cudaStream_t st);
 
+cudaError_t launch_steering(const double* xi, const double* eta, int n, int n_axes, const double* elev, const double* motion,
+                            int ms0, int ms1, long long col0, long long ncols, double sign, float2* out, int num_sms, cudaStream_t st);
+
 struct SelectParams {
   const float2* A;
   int n, m;

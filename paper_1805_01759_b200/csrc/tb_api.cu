@@ -599,6 +599,23 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   return TB_OK;
 }
 
+int tb_build_steering(int device, const double* xi_dev, const double* eta_dev, int64_t n, int32_t n_axes,
+                      const double* elev_dev, int64_t n_elev, const double* motion_dev, const int32_t* motion_sizes_host,
+                      int64_t col0, int64_t ncols, double sign, void* out_dev, void* stream) {
+  if (!xi_dev || !elev_dev || !out_dev || n < 1 || n_elev < 1 || ncols < 0) return fail(TB_ERR_INVALID, "invalid steering arguments");
+  if (n_axes < 0 || n_axes > 2 || (n_axes > 0 && (!eta_dev || !motion_dev || !motion_sizes_host)))
+    return fail(TB_ERR_INVALID, "1 elevation + at most 2 motion axes supported");
+  if (!(sign == 1.0 || sign == -1.0)) return fail(TB_ERR_INVALID, "sign must be +1 or -1");
+  const int ms0 = n_axes >= 1 ? motion_sizes_host[0] : 1, ms1 = n_axes >= 2 ? motion_sizes_host[1] : 1;
+  const long long m = n_elev * (long long)ms0 * ms1;
+  if (col0 < 0 || col0 + ncols > m) return fail(TB_ERR_INVALID, "column range [%lld, %lld) outside grid of %lld", (long long)col0, (long long)(col0 + ncols), m);
+  TB_CUDA(cudaSetDevice(device));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  TB_CUDA(tb::launch_steering(xi_dev, eta_dev, (int)n, n_axes, elev_dev, motion_dev, ms0, ms1, col0, ncols, sign, (float2*)out_dev, sms, (cudaStream_t)stream));
+  return TB_OK;
+}
+
 int tb_select(tb_ctx* c, const void* x, const void* pixels, int64_t P, int32_t n_elev, int32_t n_axes,
               const int32_t* msizes, const double* elev, const double* motion, int32_t k_max, int32_t ppsc,
               int32_t* order, int64_t* support, void* amps, double* elevs, double* motion_out, double* scores,

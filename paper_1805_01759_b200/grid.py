@@ -4,8 +4,8 @@ Mirrors the reference ``ParameterGrid`` (``model.py:154-235``): the dictionary's
 index enumerates the grid row-major with elevation as the leading axis
 (``model.py:158-160``), ``values_at`` decodes (elevation, motion coefficients)
 (``model.py:203-208``) and ``elevation_profile`` collapses motion axes by max
-(``model.py:210-215``).  Geometry/steering construction is out of scope (the dictionary is
-an input to the hot path), so only the grid description and its decode live here.
+(``model.py:210-215``).  ``build_steering_matrix`` builds the dense dictionary on the device
+(``model.py:296-323``; SURVEY section 8f "next" row 2), whole or as one rank's column shard.
 """
 
 from __future__ import annotations
@@ -102,3 +102,39 @@ class ParameterGrid:
             axes.append(np.linspace(lo, hi, count))
             bases.append(base)
         return cls(elevation=elev, motion_axes=tuple(axes), motion_bases=tuple(bases))
+
+
+def build_steering_matrix(xi, grid: ParameterGrid, eta=None, sign: float = 1.0, col_range=None, device=None):
+    """Dense steering dictionary on the device (model.py:296-323), complex64 torch tensor [n, m].
+
+    ``xi``: spatial frequencies (n,) (model.py:254-259; BASELINE uses the normalised f_i with
+    sign=-1); ``eta``: temporal frequencies (n_axes, n) (model.py:262-277), one row per motion axis.
+    ``col_range`` (start, stop) builds one column shard only.  No 50M-entry budget: the dictionary
+    lives in HBM (cfg5's 100 x 1,048,576 = 800 MiB).
+    """
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .exceptions import NumericalError
+
+    if not torch.cuda.is_available():
+        raise NumericalError("no CUDA device: the B200 solver has no CPU fallback")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+    xi_t = torch.as_tensor(np.asarray(xi, dtype=np.float64)).to(dev)
+    n = int(xi_t.numel())
+    n_axes = len(grid.motion_axes)
+    eta_np = np.zeros((max(n_axes, 1), n)) if eta is None else np.asarray(eta, dtype=np.float64).reshape(n_axes, n)
+    eta_t = torch.as_tensor(np.ascontiguousarray(eta_np)).to(dev)
+    elev_t = torch.as_tensor(np.array(grid.elevation, dtype=np.float64)).to(dev)
+    mot = np.concatenate([np.asarray(a, dtype=np.float64) for a in grid.motion_axes]) if n_axes else np.zeros(1)
+    mot_t = torch.as_tensor(mot).to(dev)
+    sizes = (ctypes.c_int32 * max(1, n_axes))(*([a.size for a in grid.motion_axes] or [1]))
+    c0, c1 = (0, grid.flat_size) if col_range is None else (int(col_range[0]), int(col_range[1]))
+    out = torch.empty((n, c1 - c0), dtype=torch.complex64, device=dev)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.tb_build_steering(dev.index, _lib.ptr(xi_t), _lib.ptr(eta_t), n, n_axes, _lib.ptr(elev_t), int(grid.elevation.size),
+                                         _lib.ptr(mot_t), sizes, c0, c1 - c0, float(sign), _lib.ptr(out), torch.cuda.current_stream(dev).cuda_stream))
+    return out

@@ -205,6 +205,16 @@ def main():
     put("msel_dup/support", sup)
     put("msel_dup/scores", sc)
 
+    # --- model.py: steering dictionary with two motion axes (model.py:254-323)
+    geom = T.demo_geometry(n_acquisitions=29, seed=7)
+    sgrid = T.ParameterGrid.uniform((-20.0, 20.0), 11, (("linear", -0.02, 0.02, 3), ("seasonal", 0.0, 0.01, 2)))
+    put("steer/xi", T.spatial_frequencies(geom))
+    put("steer/eta", T.temporal_frequencies(geom, sgrid.motion_bases))
+    put("steer/elev", sgrid.elevation)
+    put("steer/ax0", sgrid.motion_axes[0])
+    put("steer/ax1", sgrid.motion_axes[1])
+    put("steer/a", T.build_steering_matrix(geom, sgrid).entries)
+
     path = os.path.join(os.path.dirname(__file__), "golden_v1.npz")
     np.savez_compressed(path, **OUT)
     print(f"wrote {path} ({os.path.getsize(path)} bytes, {len(OUT)} arrays)")

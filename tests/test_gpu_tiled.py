@@ -203,3 +203,25 @@ def test_cfg5_selection_kmax3_vs_oracle(tb):
         np.testing.assert_allclose(est.elevations[p, :k].cpu().numpy(), ref["elevations"])
         np.testing.assert_allclose(est.motion_params[p, :k].cpu().numpy(), ref["motion_params"])
         np.testing.assert_allclose(est.selection_scores[p, : k + 1].cpu().numpy()[: len(sc)], sc[: k + 1], rtol=1e-10)
+
+
+def test_device_steering_matrix(tb, golden):
+    """On-device dictionary build vs the reference's build_steering_matrix (golden) and vs the host
+    synthesis of BASELINE cfg4 (sign -1): equal at complex64 precision."""
+    from paper_1805_01759_b200.grid import build_steering_matrix
+    from paper_1805_01759_b200.synth import WAVELENGTH, make_config
+
+    g = tb.ParameterGrid(elevation=golden["steer/elev"], motion_axes=(golden["steer/ax0"], golden["steer/ax1"]), motion_bases=("linear", "seasonal"))
+    a = build_steering_matrix(golden["steer/xi"], g, eta=golden["steer/eta"], sign=1.0).cpu().numpy()
+    ref = golden["steer/a"].astype(np.complex64)
+    assert np.max(np.abs(a - ref)) <= 2.5e-7
+    c4 = make_config(4, num_pixels=1)
+    f, t = c4.meta["freqs"], c4.meta["times"]
+    eta = np.stack([2.0 * t / WAVELENGTH, 2.0 * np.sin(2.0 * np.pi * t) / WAVELENGTH])
+    a4 = build_steering_matrix(f, c4.grid, eta=eta, sign=-1.0).cpu().numpy()
+    diff = np.abs(a4 - c4.dictionary)
+    assert diff.max() <= 2.5e-7
+    assert np.mean(a4 == c4.dictionary) > 0.999
+    # a column shard is the same columns of the full build
+    shard = build_steering_matrix(f, c4.grid, eta=eta, sign=-1.0, col_range=(1000, 5000)).cpu().numpy()
+    np.testing.assert_array_equal(shard, a4[:, 1000:5000])

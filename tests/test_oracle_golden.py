@@ -125,3 +125,14 @@ def test_model_select_rank_deficient(golden):
     assert k == int(golden["msel_dup/k"])
     assert list(sup) == list(golden["msel_dup/support"])
     np.testing.assert_allclose(sc, golden["msel_dup/scores"], rtol=1e-12)
+
+
+def test_steering_restatement_matches_reference(golden):
+    """exp(j 2 pi (xi s + eta_0 p_0 + eta_1 p_1)) row-major over the grid (model.py:296-323)."""
+    xi, eta = golden["steer/xi"], golden["steer/eta"]
+    s, p0, p1 = golden["steer/elev"], golden["steer/ax0"], golden["steer/ax1"]
+    mesh = np.meshgrid(s, p0, p1, indexing="ij")
+    phase = np.outer(xi, mesh[0].reshape(-1))
+    phase += np.outer(eta[0], mesh[1].reshape(-1))
+    phase += np.outer(eta[1], mesh[2].reshape(-1))
+    np.testing.assert_array_equal(np.exp(2j * np.pi * phase), golden["steer/a"])
