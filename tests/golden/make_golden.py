@@ -215,6 +215,42 @@ def main():
     put("steer/ax1", sgrid.motion_axes[1])
     put("steer/a", T.build_steering_matrix(geom, sgrid).entries)
 
+    # --- cli.py solve on a TSTK1 stack (the production caller, cli.py:112-174)
+    import json
+    import tempfile
+
+    from tomobpdn import cli, simulate, stack
+
+    sgeom = T.demo_geometry(n_acquisitions=29, seed=3)
+    rho = sgeom.rayleigh_resolution
+    prng = substream(99, 1)
+    rows = []
+    for p in range(24):
+        k = p % 3
+        scs = tuple(simulate.Scatterer(elevation=float(prng.uniform(-2 * rho, 2 * rho)), amplitude=float(prng.uniform(0.6, 1.4)), phase=float(prng.uniform(0, 6.28))) for _ in range(k))
+        sc = simulate.Scenario(geometry=sgeom, scatterers=scs, snr_db=tuple(10.0 for _ in scs), seed=p)
+        rows.append(simulate.synthesize_pixel(sc, substream(99, 100 + p)))
+    rows.append(np.zeros(29))
+    with tempfile.TemporaryDirectory() as td:
+        spath = os.path.join(td, "s.tstk")
+        stack.write_stack(spath, sgeom, np.array(rows))
+        put("cli/stack", np.frombuffer(open(spath, "rb").read(), dtype=np.uint8))
+        cfgp = os.path.join(td, "c.json")
+        open(cfgp, "w").write(json.dumps({"max_iters": 500, "tol": 1e-6, "seed": 77}))
+        put("cli/config", json.dumps({"max_iters": 500, "tol": 1e-6, "seed": 77}))
+        grids = {
+            "g1": {"elevation": {"min": -2 * rho, "max": 2 * rho, "count": 81}},
+            "g2": {"elevation": {"min": -2 * rho, "max": 2 * rho, "count": 41}, "motion": [{"base": "linear", "min": -0.01, "max": 0.01, "count": 5}]},
+        }
+        for gname, gd in grids.items():
+            put(f"cli/{gname}", json.dumps(gd))
+            gp = os.path.join(td, gname + ".json")
+            open(gp, "w").write(json.dumps(gd))
+            for backend in (("rbpg", "fista") if gname == "g1" else ("rbpg",)):
+                op = os.path.join(td, f"{gname}_{backend}.jsonl")
+                assert cli.main(["solve", "--stack", spath, "--grid", gp, "--out", op, "--config", cfgp, "--backend", backend, "--csv", op + ".csv"]) == 0
+                put(f"cli/{gname}_{backend}_jsonl", open(op).read())
+
     path = os.path.join(os.path.dirname(__file__), "golden_v1.npz")
     np.savez_compressed(path, **OUT)
     print(f"wrote {path} ({os.path.getsize(path)} bytes, {len(OUT)} arrays)")

@@ -109,3 +109,18 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(tb.NumericalError):
         tb.Dictionary(np.eye(3, dtype=np.complex64))
+
+
+def test_stack_format_roundtrip_and_errors(tmp_path):
+    from paper_1805_01759_b200.exceptions import StackFormatError
+    from paper_1805_01759_b200.stack import Geometry, read_stack, write_stack
+
+    g = Geometry(np.linspace(-100, 100, 5), np.linspace(0, 1, 5), 0.031, 6e5)
+    px = (np.arange(15) + 1j * np.arange(15)).reshape(3, 5).astype(np.complex64)
+    p = tmp_path / "x.tstk"
+    write_stack(p, g, px)
+    g2, px2 = read_stack(p)
+    np.testing.assert_array_equal(px2, px)
+    p.write_bytes(p.read_bytes()[:-3])
+    with pytest.raises(StackFormatError):
+        read_stack(p)
