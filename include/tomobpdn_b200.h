@@ -122,6 +122,12 @@ int tb_tiled_finish(tb_tiled* h, void* x_dev, double* f_final_dev, int32_t* iter
                     int32_t* status_dev, void* stream);
 int tb_tiled_destroy(tb_tiled* h);
 
+/* svd_wiener_solve (solver.py:393-407) batched: x_p = W b_p with the precomputed linear filter
+ * W = V diag(s / (s^2 + mu)) U^H (complex128 [m][n], from the dictionary's thin SVD); fp64
+ * accumulation, complex64 x_dev [P][m] for the selection stage. */
+int tb_apply_filter(tb_ctx* ctx, const void* filter_dev, const void* pixels_dev, int64_t num_pixels,
+                    void* x_dev, void* stream);
+
 /* build_steering_matrix (model.py:296-323) on the device: out[i, c] = exp(sign j 2 pi phase_i(col0+c))
  * with phase_i(k) = xi_i s(k) + sum_a eta_{a,i} p_a(k) over the row-major grid (elevation leading);
  * sign = +1 is the reference convention, -1 the BASELINE.json one.  Writes complex64

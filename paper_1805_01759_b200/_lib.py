@@ -53,6 +53,7 @@ SIGNATURES = {
     "tb_tiled_remaining": (c_int32, [c_void_p, ctypes.POINTER(c_int64), c_void_p]),
     "tb_tiled_finish": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "tb_tiled_destroy": (c_int32, [c_void_p]),
+    "tb_apply_filter": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "tb_build_steering": (c_int32, [c_int32, c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_void_p, ctypes.POINTER(c_int32), c_int64, c_int64, c_double, c_void_p, c_void_p]),
     "tb_select": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32, ctypes.POINTER(c_int32), c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
 }

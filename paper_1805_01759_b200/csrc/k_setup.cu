@@ -347,4 +347,47 @@ cudaError_t launch_steering(const double* xi, const double* eta, int n, int n_ax
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ linear filter apply
+// svd_wiener_solve (solver.py:393-407) with the filter W = V diag(s/(s^2+mu)) U^H precomputed:
+// x_p = W b_p for every pixel, fp64 accumulation, complex64 output for the selection stage.
+__global__ void __launch_bounds__(256) apply_filter_kernel(const double2* __restrict__ W, int n, int m,
+                                                           const float2* __restrict__ B, long long P,
+                                                           float2* __restrict__ X) {
+  extern __shared__ double2 sbd[];  // [warps][n]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double2* bw = sbd + (size_t)warp * n;
+  for (long long p = (long long)blockIdx.x * nw + warp; p < P; p += (long long)gridDim.x * nw) {
+    for (int i = lane; i < n; i += 32) {
+      const float2 b = B[(size_t)p * n + i];
+      bw[i] = make_double2(b.x, b.y);
+    }
+    __syncwarp();
+    for (int c = lane; c < m; c += 32) {
+      double re = 0.0, im = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double2 w = __ldg(&W[(size_t)c * n + i]);
+        const double2 b = bw[i];
+        re = fma(w.x, b.x, fma(-w.y, b.y, re));
+        im = fma(w.x, b.y, fma(w.y, b.x, im));
+      }
+      X[(size_t)p * m + c] = make_float2((float)re, (float)im);
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_apply_filter(const double2* W, int n, int m, const float2* B, long long P, float2* X, int num_sms, cudaStream_t st) {
+  if (P <= 0) return cudaSuccess;
+  const int warps = 8;
+  long long blocks = (P + warps - 1) / warps;
+  if (blocks > (long long)num_sms * 8) blocks = (long long)num_sms * 8;
+  const size_t smem = (size_t)warps * n * sizeof(double2);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(apply_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  apply_filter_kernel<<<(int)blocks, warps * 32, smem, st>>>(W, n, m, B, P, X);
+  return cudaGetLastError();
+}
+
 }  // namespace tb

@@ -19,6 +19,8 @@ cudaError_t power_iter_large(const float2* A, int n, int m, long long start, lon
 cudaError_t launch_steering(const double* xi, const double* eta, int n, int n_axes, const double* elev, const double* motion,
                             int ms0, int ms1, long long col0, long long ncols, double sign, float2* out, int num_sms, cudaStream_t st);
 
+cudaError_t launch_apply_filter(const double2* W, int n, int m, const float2* B, long long P, float2* X, int num_sms, cudaStream_t st);
+
 struct SelectParams {
   const float2* A;
   int n, m;

@@ -599,6 +599,14 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   return TB_OK;
 }
 
+int tb_apply_filter(tb_ctx* c, const void* filter_dev, const void* pixels_dev, int64_t P, void* x_dev, void* stream) {
+  if (!c || (P > 0 && (!filter_dev || !pixels_dev || !x_dev))) return fail(TB_ERR_INVALID, "null argument");
+  if (P < 0) return fail(TB_ERR_INVALID, "num_pixels must be >= 0");
+  TB_CUDA(cudaSetDevice(c->device));
+  TB_CUDA(tb::launch_apply_filter((const double2*)filter_dev, (int)c->n, (int)c->m, (const float2*)pixels_dev, P, (float2*)x_dev, c->num_sms, (cudaStream_t)stream));
+  return TB_OK;
+}
+
 int tb_build_steering(int device, const double* xi_dev, const double* eta_dev, int64_t n, int32_t n_axes,
                       const double* elev_dev, int64_t n_elev, const double* motion_dev, const int32_t* motion_sizes_host,
                       int64_t col0, int64_t ncols, double sign, void* out_dev, void* stream) {

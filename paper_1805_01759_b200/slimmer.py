@@ -144,10 +144,11 @@ def pipeline_batch(dictionary, pixels, grid: ParameterGrid, config: PipelineConf
     derive_seed(substream(run_seed, first_pixel_id + i)) with run_seed = config.solver.seed
     (cli.py:102, 125).
     """
-    if config.backend == "svd_wiener":
-        raise ConfigurationError("svd_wiener is not part of the B200 solver path (see DESIGN.md scope)")
     d = dictionary if isinstance(dictionary, Dictionary) else Dictionary(dictionary, device=device)
     b = d._pixels(pixels)
+    if config.backend == "svd_wiener":  # slimmer.py:198-199: linear estimator, then the same selection
+        est = select_batch(d, d.wiener(b, config.wiener_mu), b, grid, config.k_max)
+        return est
     p = int(b.shape[0])
     if lam is None:
         lam_t = d.default_lambda(b, beta) if config.solver.lambda_reg is None else None
@@ -166,9 +167,9 @@ def pipeline_batch(dictionary, pixels, grid: ParameterGrid, config: PipelineConf
 
 def slimmer_pipeline(obj: Objective, grid: ParameterGrid, config: PipelineConfig) -> ScattererEstimates:
     """Run sparse solve, model selection, and debiasing for one pixel (slimmer.py:193-212)."""
-    if config.backend == "svd_wiener":
-        raise ConfigurationError("svd_wiener is not part of the B200 solver path (see DESIGN.md scope)")
     d = dictionary_for(obj.dictionary)
+    if config.backend == "svd_wiener":
+        return select_batch(d, d.wiener(obj.measurement.reshape(1, -1), config.wiener_mu), obj.measurement.reshape(1, -1), grid, config.k_max).estimates(0)
     seeds = np.array([int(config.solver.seed) & (2**64 - 1)], dtype=np.uint64) if config.backend == "rbpg" else None
     sol = d.solve(obj.measurement.reshape(1, -1), np.array([obj.lambda_reg]), config.solver, config.backend, seeds=seeds)
     est = select_batch(d, sol.x_hat, obj.measurement.reshape(1, -1), grid, config.k_max)

@@ -400,6 +400,36 @@ class Dictionary:
         return res
 
 
+    def wiener_filter(self, noise_power: float):
+        """W = V diag(s / (s^2 + mu)) U^H from the thin SVD of A (solver.py:393-407), cached per mu.
+
+        The SVD (cuSOLVER, complex128, n x m with n <= 128) is a once-per-dictionary setup step on
+        the device; applying W to the pixel stack is the batched kernel ``tb_apply_filter``.
+        """
+        torch = _torch()
+        if not (np.isfinite(noise_power) and noise_power >= 0):
+            raise ConfigurationError(f"noise_power must be >= 0, got {noise_power}")
+        cache = self.__dict__.setdefault("_wiener", {})
+        if noise_power not in cache:
+            try:
+                u, s, vh = torch.linalg.svd(self.tensor.to(torch.complex128), full_matrices=False)
+            except RuntimeError as exc:
+                raise NumericalError(f"SVD failed: {exc}") from exc
+            filt = s / (s * s + noise_power)
+            cache[noise_power] = (vh.conj().transpose(0, 1) * filt.to(torch.complex128)[None, :]) @ u.conj().transpose(0, 1)
+            cache[noise_power] = cache[noise_power].contiguous()
+        return cache[noise_power]
+
+    def wiener(self, pixels, noise_power: float):
+        """svd_wiener_solve for every pixel: complex64 x_hat [P, m] (solver.py:393-407)."""
+        torch = _torch()
+        w = self.wiener_filter(noise_power)
+        b = self._pixels(pixels)
+        x = torch.empty((b.shape[0], self.m), dtype=torch.complex64, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.tb_apply_filter(self._h, _lib.ptr(w), _lib.ptr(b), b.shape[0], _lib.ptr(x), self._stream()))
+        return x
+
     def _solve_tiled(self, backend, cfg, b, lam_t, seeds_t, p, x, ffin, hist, total, its, st, allreduce):
         torch = _torch()
         if p == 0:
@@ -506,6 +536,11 @@ def sample_block(partition: BlockPartition, rng) -> int:
     return int(rng.choice(partition.num_blocks, p=partition.probabilities))
 
 
-def svd_wiener_solve(obj, noise_power: float):
-    """Out of scope for the B200 hot path ('next' row 4)."""
-    raise ConfigurationError("svd_wiener is not part of the B200 solver path (see DESIGN.md scope)")
+def svd_wiener_solve(obj, noise_power: float) -> np.ndarray:
+    """Wiener/Tikhonov-regularised pseudo-inverse profile V diag(s/(s^2+mu)) U^H g (solver.py:393-407)."""
+    from .prox import Objective
+
+    if not isinstance(obj, Objective):
+        raise ConfigurationError("expected an Objective")
+    d = dictionary_for(obj.dictionary)
+    return d.wiener(obj.measurement.reshape(1, -1), noise_power)[0].cpu().numpy().astype(np.complex128)

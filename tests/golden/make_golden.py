@@ -215,6 +215,21 @@ def main():
     put("steer/ax1", sgrid.motion_axes[1])
     put("steer/a", T.build_steering_matrix(geom, sgrid).entries)
 
+    # --- svd_wiener backend (solver.py:393-407, slimmer.py:198-199)
+    for mu in (0.0, 2.5):
+        xs, orders, sups = [], [], []
+        for p in range(npx):
+            obj = T.Objective(dictionary=a, measurement=pix[p].astype(np.complex128), lambda_reg=0.0)
+            xs.append(T.svd_wiener_solve(obj, mu))
+            est = T.slimmer_pipeline(obj, grid, T.PipelineConfig(backend="svd_wiener", wiener_mu=mu, k_max=2))
+            orders.append(est.model_order)
+            sp = np.full(2, -1)
+            sp[: est.support.size] = est.support
+            sups.append(sp)
+        put(f"wiener{mu}/x", np.array(xs))
+        put(f"wiener{mu}/order", np.array(orders))
+        put(f"wiener{mu}/support", np.array(sups))
+
     # --- cli.py solve on a TSTK1 stack (the production caller, cli.py:112-174)
     import json
     import tempfile

@@ -225,3 +225,19 @@ def test_large_batch_properties(tb):
     f0 = (b.abs() ** 2).sum(dim=1).double()
     assert bool((r.objective_final <= f0 * (1 + 1e-6)).all())
     assert bool(torch.isfinite(r.x_hat).all())
+
+
+@pytest.mark.parametrize("mu", [0.0, 2.5])
+def test_svd_wiener_backend(tb, golden, cfg1, mu):
+    """Batched svd_wiener (device SVD filter + apply kernel) and its pipeline vs the reference."""
+    pix = golden["cfg1/b"]
+    x = cfg1.wiener(pix, mu).cpu().numpy()
+    ref = golden[f"wiener{mu}/x"]
+    err = np.linalg.norm(x - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert err.max() <= 1e-5
+    grid = tb.ParameterGrid(elevation=golden["cfg1/elev"])
+    est = tb.pipeline_batch(cfg1, pix, grid, tb.PipelineConfig(backend="svd_wiener", wiener_mu=mu, k_max=2))
+    assert np.array_equal(est.support.cpu().numpy(), golden[f"wiener{mu}/support"])
+    assert np.array_equal(est.model_order.cpu().numpy(), golden[f"wiener{mu}/order"])
+    obj = tb.Objective(dictionary=golden["cfg1/a"].astype(np.complex128), measurement=pix[0], lambda_reg=0.0)
+    np.testing.assert_allclose(tb.svd_wiener_solve(obj, mu), ref[0], rtol=1e-5, atol=1e-6)

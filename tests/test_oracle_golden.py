@@ -136,3 +136,19 @@ def test_steering_restatement_matches_reference(golden):
     phase += np.outer(eta[0], mesh[1].reshape(-1))
     phase += np.outer(eta[1], mesh[2].reshape(-1))
     np.testing.assert_array_equal(np.exp(2j * np.pi * phase), golden["steer/a"])
+
+
+@pytest.mark.parametrize("mu", [0.0, 2.5])
+def test_svd_wiener(golden, mu):
+    a = golden["cfg1/a"].astype(np.complex128)
+    pix = golden["cfg1/b"]
+
+    class G:
+        elevation = golden["cfg1/elev"]
+        motion_axes = ()
+        shape = (a.shape[1],)
+
+    for p in range(pix.shape[0]):
+        np.testing.assert_allclose(O.svd_wiener(a, pix[p], mu), golden[f"wiener{mu}/x"][p], rtol=1e-9, atol=1e-12)
+        est = O.pipeline(a, pix[p].astype(np.complex128), mu, G, 2, "svd_wiener", None)
+        assert list(est["support"]) == [int(v) for v in golden[f"wiener{mu}/support"][p] if v >= 0]
