@@ -145,7 +145,7 @@ int tb_spectral_sq_norms(tb_ctx* c, int32_t num_ranges, const int64_t* starts, c
   TB_CUDA(cudaMallocAsync(&out, sizeof(double) * num_ranges, st));
   TB_CUDA(cudaMemcpyAsync(v, v0_dev, sizeof(double2) * total, cudaMemcpyDeviceToDevice, st));
   // small ranges on one CTA each (whole loop on device), wide ranges host-driven multi-CTA
-  const long long small_limit = 1ll << 22;
+  const long long small_limit = 1ll << 18;  // wider ranges use the multi-CTA path (one CTA per range is too slow for cfg4/5 blocks)
   std::vector<long long> ss, se;
   std::vector<int> small_idx;
   std::vector<long long> offs(num_ranges);
