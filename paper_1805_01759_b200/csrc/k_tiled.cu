@@ -136,12 +136,13 @@ __global__ void __launch_bounds__(1024) tiled_schedule_kernel(const TiledParams 
 
 // ------------------------------------------------------------------ fused pass
 constexpr int TL_AS = TL_CT + 1;  // odd row stride of the staged A tile
+constexpr int TL_ZS = TL_PT + 1;  // padded row stride of the staged candidate tile (conflict-free epilogue stores)
 
 __host__ __device__ inline size_t tiled_pass_smem(int n) {
   size_t b = (size_t)n * TL_PT * 8;               // sRY
   b += (size_t)n * TL_AS * 8;                     // sA
   b = (b + 15) & ~(size_t)15;
-  b += (size_t)TL_CT * TL_PT * 16;                // sZ
+  b += (size_t)TL_CT * TL_ZS * 16;                // sZ
   b += TL_CT * 4;                                 // sFlag
   b += TL_PT * (4 * 8 + 4 * 4);                   // per-pixel scalars
   return (b + 15) & ~(size_t)15;
@@ -163,8 +164,8 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
   float2* sRY = reinterpret_cast<float2*>(sm);  // [n][PT]
   float2* sA = sRY + (size_t)n * TL_PT;         // [n][TL_AS]
   size_t o = ((size_t)n * TL_PT * 8 + (size_t)n * TL_AS * 8 + 15) & ~(size_t)15;
-  double2* sZ = reinterpret_cast<double2*>(sm + o);  // [CT][PT]
-  int* sFlag = reinterpret_cast<int*>(sZ + TL_CT * TL_PT);
+  double2* sZ = reinterpret_cast<double2*>(sm + o);  // [CT][ZS]
+  int* sFlag = reinterpret_cast<int*>(sZ + TL_CT * TL_ZS);
   double* sAlpha = reinterpret_cast<double*>(sFlag + TL_CT);
   double* sTau = sAlpha + TL_PT;
   double* sMk = sTau + TL_PT;
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
           w = rb ? d : z;
           if (w.x != 0.0 || w.y != 0.0) sFlag[c] = 1;
         }
-        sZ[c * TL_PT + slot] = w;
+        sZ[c * TL_ZS + slot] = w;
       }
     }
     __syncthreads();
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
       const double ax = af.x, ayv = af.y;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        const double2 z = sZ[c * TL_PT + fph + q];
+        const double2 z = sZ[c * TL_ZS + fph + q];
         facc[q].x = fma(ax, z.x, fma(-ayv, z.y, facc[q].x));
         facc[q].y = fma(ax, z.y, fma(ayv, z.x, facc[q].y));
       }
