@@ -24,7 +24,7 @@
 #include "solver_params.h"
 
 #ifndef TB_WARP_LB
-#define TB_WARP_LB 448
+#define TB_WARP_LB 512
 #endif
 
 namespace tb {
@@ -61,9 +61,6 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kern
   __syncthreads();
   off += block_table_bytes(J);
   const double alpha0_full = P.alpha_scale / fmax(P.lip_full, 1e-300);  // solver.py:345
-  double cdf_r[7];
-#pragma unroll
-  for (int q = 0; q < 7; ++q) cdf_r[q] = (RB && q < J) ? s_cdf[q] : 2.0;
   const size_t per_warp = warp_slot_bytes(n, m, P.max_width, J);
   unsigned char* wb = smem + off + (size_t)warp * per_warp;
   double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA)
@@ -138,8 +135,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kern
       for (int j = lane; j < J; j += 32) l1blk[j] = 0.0;
     if (lane == 0) ring[0] = F;
     if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
-    Philox4x64 rng;
-    if (RB) philox_init(rng, P.seeds[p], 0ull);
+    const uint64_t seed = RB ? P.seeds[p] : 0ull;
+    uint64_t* rbuf = reinterpret_cast<uint64_t*>(ring + 12);  // 4 buffered Philox outputs
     int status = STATUS_MAX_ITERS;
     int iters = 0;
     bool stopped = false;
@@ -150,12 +147,20 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kern
       // ---- block choice (solver.py:283, 217-219): searchsorted(cdf, u, 'right')
       int blk = 0, cs = 0, ce = m;
       if (RB) {
-        double u = raw_to_unit(philox_next(rng));
+        // raw draw k-1 of Philox(key=[seed, 0]): counter (k-1)/4 + 1, output (k-1) % 4
+        const int w = (k - 1) & 3;
+        if (w == 0) {
+          uint64_t c4[4] = {(uint64_t)((k - 1) >> 2) + 1ull, 0ull, 0ull, 0ull};
+          philox4x64_10(c4, seed, 0ull);
+          if (lane < 4) rbuf[lane] = lane == 0 ? c4[0] : lane == 1 ? c4[1] : lane == 2 ? c4[2] : c4[3];
+          __syncwarp();
+        }
+        const double u = raw_to_unit(rbuf[w]);
         int j = 0;
         if (J <= 8) {
           // searchsorted(cdf, u, 'right') with cdf[J-1] == 1 > u: count of cdf[j] <= u, j < J-1
 #pragma unroll
-          for (int q = 0; q < 7; ++q) j += (q < J - 1 && cdf_r[q] <= u) ? 1 : 0;
+          for (int q = 0; q < 7; ++q) j += (q < J - 1 && s_cdf[q] <= u) ? 1 : 0;
         } else {
           while (j < J - 1 && s_cdf[j] <= u) ++j;
         }
