@@ -23,6 +23,9 @@
 #include "common.cuh"
 #include "solver_params.h"
 
+#ifndef TB_WARP_LB_WIDE
+#define TB_WARP_LB_WIDE 384
+#endif
 #ifndef TB_WARP_LB
 #define TB_WARP_LB 512
 #endif
@@ -30,7 +33,7 @@
 namespace tb {
 
 template <bool RB, int MAXT, int MAXQ, bool ASMEM>
-__global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kernel(const SolveParams P) {
+__global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp_solver_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -172,7 +175,6 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kern
       const double mk = ista ? 0.0 : P.mk[k];  // (k-2)/(k+1), host table (solver.py:222-224)
 
       // ---- extrapolation y = x + m_k (x - prev) (solver.py:288-289, 356)
-      double2 y[MAXT];
       float2 g[MAXT];
       double2 z[RB ? MAXT : 1];
       unsigned masks[MAXT];
@@ -180,7 +182,6 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kern
 #pragma unroll
       for (int t = 0; t < MAXT; ++t) {
         const int cl = lane + 32 * t;
-        y[t] = make_double2(0.0, 0.0);
         bool nz = false;
         if (cl < width) {
           const double2 xv = xs[cs + cl];
@@ -192,7 +193,6 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kern
             yv.x = fma(mk, (double)dv.x, xv.x);
             yv.y = fma(mk, (double)dv.y, xv.y);
           }
-          y[t] = yv;
           if (RB) {
             const double2 dy = make_double2(yv.x - xv.x, yv.y - xv.y);
             zs[cl] = dy;
@@ -274,7 +274,15 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kern
           const int cl = lane + 32 * t;
           bool nz = false;
           if (cl < width) {
-            const double2 v = make_double2(fma(-alpha, (double)g[t].x, y[t].x), fma(-alpha, (double)g[t].y, y[t].y));
+            // y = x + m_k d recomputed from shared memory (keeps registers for occupancy)
+            const double2 xv = xs[cs + cl];
+            double2 yv = xv;
+            if (!ista) {
+              const float2 dv = ds[cs + cl];
+              yv.x = fma(mk, (double)dv.x, xv.x);
+              yv.y = fma(mk, (double)dv.y, xv.y);
+            }
+            const double2 v = make_double2(fma(-alpha, (double)g[t].x, yv.x), fma(-alpha, (double)g[t].y, yv.y));
             const double mag2 = fma(v.x, v.x, v.y * v.y);
             double2 zz = make_double2(0.0, 0.0);
             if (mag2 > tau2) {  // soft_threshold: zero iff |v| <= tau (prox.py:82-96)
@@ -284,7 +292,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? 256 : TB_WARP_LB) warp_solver_kern
               red[1] += mag * sc;
             }
             if (RB) z[t] = zz;
-            const double2 d = make_double2(zz.x - y[t].x, zz.y - y[t].y);
+            const double2 d = make_double2(zz.x - yv.x, zz.y - yv.y);
             red[0] += fma(d.x, d.x, d.y * d.y);
             const double2 w = RB ? d : zz;
             zs[cl] = w;
@@ -473,7 +481,7 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   const size_t tables = block_table_bytes(J);
   const size_t a_bytes = ((size_t)P.n * P.ms * sizeof(float2) + 15) & ~(size_t)15;
   const size_t cap = 227 * 1024;
-  const int max_warps = maxt >= 8 ? 8 : TB_WARP_LB / 32;
+  const int max_warps = maxt >= 8 ? TB_WARP_LB_WIDE / 32 : TB_WARP_LB / 32;
   bool asmem = a_bytes + tables + 4 * slot <= cap;
   size_t avail = cap - tables - (asmem ? a_bytes : 0);
   int warps = (int)(avail / slot);
