@@ -403,15 +403,8 @@ __global__ void tiled_update_kernel(const TiledParams T) {
       const double l1_new = T.l1[p] - T.l1blk[(size_t)p * T.J + b] + zsum;
       const double cand = fz + lamd * l1_new;
       const bool accept = cand <= F;  // solver.py:317-325
-      const int c0 = T.bstart[b], c1 = T.bstart[b + 1];
-      double2* xr = xrow(T, T.roles[3 * p + 0], p);
-      double2* pr = xrow(T, T.roles[3 * p + 1], p);
-      const double2* zr = xrow(T, T.roles[3 * p + 2], p);
-      for (int c = c0 + lane; c < c1; c += 32) {
-        const double2 xv = xr[c];
-        pr[c] = xv;
-        if (accept) xr[c] = zr[c];
-      }
+      // block copies prev_b <- x_b (and x_b <- z_b on accept) run in tiled_commit_kernel
+      if (lane == 0) T.commit[p] = accept ? 2 : 1;
       for (int i = lane; i < n; i += 32) {
         const size_t o = (size_t)p * n + i;
         double2* dl = T.delta + ((size_t)p * T.J + b) * n + i;
@@ -477,17 +470,39 @@ __global__ void tiled_update_kernel(const TiledParams T) {
   }
 }
 
+// ------------------------------------------------------------------ commit (RBPG)
+// prev_b <- x_b for every pixel that finished a visit this round, x_b <- z_b if it was accepted
+// (solver.py:318-325); grid over (pixel, column chunk) so wide blocks copy at HBM bandwidth.
+__global__ void tiled_commit_kernel(const TiledParams T) {
+  const int p = blockIdx.x;
+  const int flag = T.commit[p];
+  if (flag == 0) return;
+  const int b = T.blk[p];
+  const int c0 = T.bstart[b], c1 = T.bstart[b + 1];
+  double2* xr = xrow(T, T.roles[3 * p + 0], p);
+  double2* pr = xrow(T, T.roles[3 * p + 1], p);
+  const double2* zr = xrow(T, T.roles[3 * p + 2], p);
+  for (int c = c0 + blockIdx.y * blockDim.x + threadIdx.x; c < c1; c += gridDim.y * blockDim.x) {
+    const double2 xv = xr[c];
+    pr[c] = xv;
+    if (flag == 2) xr[c] = zr[c];
+  }
+}
+
+__global__ void tiled_commit_clear_kernel(const TiledParams T) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < T.P) T.commit[p] = 0;
+}
+
 // ------------------------------------------------------------------ finish
 __global__ void tiled_finish_kernel(const TiledParams T) {
-  const int lane = threadIdx.x & 31;
-  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (p >= T.P) return;
+  const int p = blockIdx.x;
   const double2* xr = xrow(T, T.roles[3 * p + 0], p);
-  for (int c = lane; c < T.m; c += 32) {
+  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < T.m; c += gridDim.y * blockDim.x) {
     const double2 v = xr[c];
     T.X[(size_t)p * T.m + c] = make_float2((float)v.x, (float)v.y);
   }
-  if (lane == 0) {
+  if (blockIdx.y == 0 && threadIdx.x == 0) {
     T.f_final[p] = T.F[p];
     T.iters[p] = T.k[p];
   }
@@ -524,12 +539,26 @@ cudaError_t tiled_reduce(const TiledParams& T, cudaStream_t st) {
 }
 
 cudaError_t tiled_update(const TiledParams& T, cudaStream_t st) {
+  const bool rb = T.mode == SOLVER_RBPG;
+  if (rb) tiled_commit_clear_kernel<<<(T.P + 255) / 256, 256, 0, st>>>(T);
   tiled_update_kernel<<<warp_grid(T.P), 256, 0, st>>>(T);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !rb) return e;
+  int maxw = 0;
+  // widest block (host copy of the starts is not kept here; bound by m / J rounded up)
+  maxw = (T.m + T.J - 1) / T.J + 1;
+  int chunks = (maxw + 2047) / 2048;  // ~8 columns per thread
+  chunks = chunks < 1 ? 1 : chunks > 64 ? 64 : chunks;
+  dim3 grid(T.P, chunks);
+  tiled_commit_kernel<<<grid, 256, 0, st>>>(T);
   return cudaGetLastError();
 }
 
 cudaError_t tiled_finish(const TiledParams& T, cudaStream_t st) {
-  tiled_finish_kernel<<<warp_grid(T.P), 256, 0, st>>>(T);
+  int chunks = (T.m + 2047) / 2048;
+  chunks = chunks < 1 ? 1 : chunks > 64 ? 64 : chunks;
+  dim3 grid(T.P, chunks);
+  tiled_finish_kernel<<<grid, 256, 0, st>>>(T);
   return cudaGetLastError();
 }
 

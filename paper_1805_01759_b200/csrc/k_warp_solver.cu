@@ -19,6 +19,7 @@
 // is evaluated in its cancellation-free algebraic form ||A d||^2 <= ||d||^2 / (2 alpha), which is
 // exactly the reference inequality f(z) <= f(y) + Re<grad, d> + ||d||^2/(2 alpha) for quadratic f.
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "solver_params.h"
@@ -486,6 +487,12 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   size_t avail = cap - tables - (asmem ? a_bytes : 0);
   int warps = (int)(avail / slot);
   if (warps > max_warps) warps = max_warps;
+  if (!asmem) {
+    // dictionary read through L1/L2: leave part of the unified L1 for A (TB_WARPS_L1 overrides)
+    const char* ev = getenv("TB_WARPS_L1");
+    const int cap_l1 = ev ? atoi(ev) : warps;
+    if (cap_l1 >= 1 && cap_l1 < warps) warps = cap_l1;
+  }
   if (warps < 1) return cudaErrorInvalidValue;
   size_t smem = (asmem ? a_bytes : 0) + tables + (size_t)warps * slot;
   long long need = (P.num_pixels + warps - 1) / warps;

@@ -343,7 +343,7 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   int ns = 0;
   sz[ns++] = align256(sizeof(double2) * 3ull * P * m);   // X3
   sz[ns++] = align256(sizeof(int) * P * 6);              // phase k trial status blk perm
-  sz[ns++] = align256(sizeof(int) * P * 3);              // roles
+  sz[ns++] = align256(sizeof(int) * P * 4);              // roles, commit
   sz[ns++] = align256(sizeof(double) * P * 3);           // F l1 alpha
   sz[ns++] = align256(sizeof(double) * P * 16);          // ring
   sz[ns++] = align256(sizeof(double) * P * J);           // l1blk
@@ -382,6 +382,7 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   T.blk = ints + 4 * P;
   T.perm = ints + 5 * P;
   T.roles = (int*)take(0);
+  T.commit = T.roles + 3 * P;
   double* dbl = (double*)take(0);
   T.F = dbl;
   T.l1 = dbl + P;

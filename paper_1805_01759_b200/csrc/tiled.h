@@ -42,6 +42,7 @@ struct TiledParams {
   int* status;
   int* blk;
   int* roles;     // [P][3]: buffer index of x, prev, z
+  int* commit;    // [P]: RBPG block copy after the round (0 none, 1 prev<-x, 2 also x<-z)
   double* F;
   double* l1;
   double* alpha;
