@@ -191,11 +191,13 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
     }
   }
   __syncthreads();
-  for (int idx = tid; idx < n * TL_PT; idx += TL_THREADS) {
-    const int i = idx / TL_PT, q = idx - i * TL_PT;
-    const int p = sPid[q];
-    sRY[idx] = p >= 0 ? T.ry32[(size_t)p * n + i] : make_float2(0.f, 0.f);
-  }
+  const bool tc = T.G != nullptr;  // adjoint precomputed on the tensor cores (k_tc_tiled.cu)
+  if (!tc)
+    for (int idx = tid; idx < n * TL_PT; idx += TL_THREADS) {
+      const int i = idx / TL_PT, q = idx - i * TL_PT;
+      const int p = sPid[q];
+      sRY[idx] = p >= 0 ? T.ry32[(size_t)p * n + i] : make_float2(0.f, 0.f);
+    }
 
   // adjoint/epilogue mapping: 16 column groups x 16 pixel pairs
   const int cg = tid & 15, pg = tid >> 4;
@@ -223,6 +225,17 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
     for (int q = 0; q < 2; ++q)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[q][j] = make_float2(0.f, 0.f);
+    if (tc) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int p = sPid[2 * pg + q];
+        if (p < 0) continue;
+        const float2* g = T.G + (size_t)p * m + col0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (cg + 16 * j < ncols) acc[q][j] = g[cg + 16 * j];
+      }
+    } else
     for (int i = 0; i < n; ++i) {
       const float4 r2 = *reinterpret_cast<const float4*>(&sRY[i * TL_PT + 2 * pg]);
       const float2 ra = make_float2(r2.x, r2.y), rbv = make_float2(r2.z, r2.w);

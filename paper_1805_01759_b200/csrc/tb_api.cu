@@ -40,7 +40,20 @@ struct tb_tiled {
   bool own_red = false;
   int max_width = 0;
   long long rounds = 0;
+  // tensor-core adjoint (k_tc_tiled.cu); G == nullptr selects the SIMT adjoint inside the pass
+  float2* G = nullptr;
+  float* Apk = nullptr;
+  float* Rpk = nullptr;
+  int* tile_base = nullptr;
+  int nck = 0, tc_max_tiles = 0, tc_tiles_per_split = 1, tc_splits = 1;
 };
+
+// TB_TILED_TC=0/1 overrides the default adjoint engine of the tiled path
+static bool tiled_use_tc() {
+  const char* e = getenv("TB_TILED_TC");
+  if (e && *e) return atoi(e) != 0;
+  return false;
+}
 
 static thread_local std::string g_err;
 
@@ -357,6 +370,20 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   sz[ns++] = red_dev ? 0 : align256(sizeof(double) * P * (2 * n + 4));  // red + redsc
   sz[ns++] = align256(sizeof(double) * J * 2);           // alpha0, cdf
   sz[ns++] = align256(sizeof(int) * (J + 1));            // bstart
+  // tensor-core adjoint: packed dictionary, packed r_y, G = A^H r_y, tile bases
+  const bool tc = tiled_use_tc();
+  std::vector<int> tc_base(J + 1, 0);
+  const int nck = tb::tc_chunks(n);
+  long long tc_total = 0;
+  if (tc) {
+    std::vector<int> hb0(J + 1);
+    for (int j = 0; j <= J; ++j) hb0[j] = rb ? c->bstart_host[j] : (j == 0 ? 0 : (int)m);
+    tc_total = tb::tc_tiles_for(hb0.data(), J, tc_base.data());
+  }
+  sz[ns++] = tc ? align256(sizeof(float) * tb::tc_dictionary_floats(tc_total, nck)) : 0;  // Apk
+  sz[ns++] = tc ? align256(sizeof(float) * tb::tc_pixel_floats(tiles, nck)) : 0;          // Rpk
+  sz[ns++] = tc ? align256(sizeof(float2) * (size_t)P * m) : 0;                          // G
+  sz[ns++] = tc ? align256(sizeof(int) * (J + 1)) : 0;                                   // tile_base
   size_t tot = 0;
   for (int i = 0; i < ns; ++i) tot += sz[i];
   size_t fr = 0, tt = 0;
@@ -410,6 +437,20 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   T.alpha0 = tabs;
   T.cdf = tabs + J;
   T.bstart = bst;
+  if (tc) {
+    h->Apk = (float*)take(0);
+    h->Rpk = (float*)take(0);
+    h->G = (float2*)take(0);
+    h->tile_base = (int*)take(0);
+    h->nck = nck;
+    h->tc_max_tiles = (int)tiles;
+    const long long ntb = (maxw + 127) / 128;
+    long long tps = (tiles * ntb + 4ll * c->num_sms - 1) / (4ll * c->num_sms);
+    if (tps < 1) tps = 1;
+    h->tc_tiles_per_split = (int)tps;
+    h->tc_splits = (int)((ntb + tps - 1) / tps);
+    T.G = h->G;
+  }
   // block tables: alpha0 = scale / max(L, 1e-300) (solver.py:295, 345), cdf, starts
   std::vector<double> ht(2 * J);
   std::vector<int> hb(J + 1);
@@ -427,6 +468,10 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   for (int j = 0; j < J; ++j) ht[J + j] = cdf[j];
   TB_CUDA(cudaMemcpyAsync(tabs, ht.data(), sizeof(double) * 2 * J, cudaMemcpyHostToDevice, st));
   TB_CUDA(cudaMemcpyAsync(bst, hb.data(), sizeof(int) * (J + 1), cudaMemcpyHostToDevice, st));
+  if (tc) {
+    TB_CUDA(cudaMemcpyAsync(h->tile_base, tc_base.data(), sizeof(int) * (J + 1), cudaMemcpyHostToDevice, st));
+    TB_CUDA(tb::tc_pack_dictionary(c->A, n, (int)m, J, bst, h->tile_base, nck, h->Apk, tc_total, c->num_sms, st));
+  }
   T.A = c->A;
   T.n = n;
   T.m = (int)m;
@@ -461,6 +506,9 @@ int tb_tiled_round_a(tb_tiled* h, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TB_CUDA(cudaSetDevice(h->ctx->device));
   TB_CUDA(tb::tiled_prep(h->T, st));
+  if (h->G)
+    TB_CUDA(tb::tc_adjoint_round(h->T, h->Apk, h->Rpk, h->tile_base, h->nck, h->tc_max_tiles, h->tc_tiles_per_split,
+                                 h->tc_splits, h->G, st));
   TB_CUDA(tb::tiled_pass(h->T, h->ctx->num_sms, st));
   TB_CUDA(tb::tiled_reduce(h->T, st));
   return TB_OK;
@@ -510,7 +558,7 @@ static int solve_tiled(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, c
   // pixel chunks sized to the free HBM (state is 3 fp64 copies of x per pixel)
   size_t fr = 0, tt = 0;
   TB_CUDA(cudaMemGetInfo(&fr, &tt));
-  const double per_px = 3.0 * 16.0 * (double)c->m + 64.0 * c->n * (solver == TB_SOLVER_RBPG ? c->num_blocks + 4 : 5) + 4096;
+  const double per_px = (tiled_use_tc() ? 56.0 : 48.0) * (double)c->m + 64.0 * c->n * (solver == TB_SOLVER_RBPG ? c->num_blocks + 4 : 5) + 4096;
   long long chunk = (long long)(0.6 * (double)fr / per_px);
   if (chunk < 1) return fail(TB_ERR_CAPACITY, "not enough device memory for one pixel of m = %lld", (long long)c->m);
   if (chunk > 8192) chunk = 8192;

@@ -53,6 +53,7 @@ struct TiledParams {
   double2* ry;    // [P][n]  fp64 r_y (RBPG) / A y (FISTA)
   double2* delta; // [P][J][n] RBPG A_b (x_b - prev_b)
   float2* ry32;   // [P][n]  r_y rounded, adjoint operand
+  const float2* G; // [P][m]  A^H r_y from the tensor-core adjoint, or null (SIMT adjoint in the pass)
   // scheduling
   int* perm;      // [P] pending pixels grouped by block
   int4* tiles;    // [P/PT + J]: (block, perm offset, count, 0)
@@ -77,5 +78,15 @@ cudaError_t tiled_pass(const TiledParams& T, int num_sms, cudaStream_t st);
 cudaError_t tiled_reduce(const TiledParams& T, cudaStream_t st);
 cudaError_t tiled_update(const TiledParams& T, cudaStream_t st);
 cudaError_t tiled_finish(const TiledParams& T, cudaStream_t st);
+
+// tensor-core adjoint (k_tc_tiled.cu)
+long long tc_tiles_for(const int* bstart_host, int J, int* tile_base_host);
+size_t tc_dictionary_floats(long long total_tiles, int nck);
+size_t tc_pixel_floats(long long max_tiles, int nck);
+int tc_chunks(int n);
+cudaError_t tc_pack_dictionary(const float2* A, int n, int m, int J, const int* bstart_dev, const int* tile_base_dev, int nck,
+                               float* Apk, long long total_tiles, int num_sms, cudaStream_t st);
+cudaError_t tc_adjoint_round(const TiledParams& T, const float* Apk, float* Rpk, const int* tile_base_dev, int nck,
+                             int max_tiles, int tiles_per_split, int max_splits, float2* G, cudaStream_t st);
 
 }  // namespace tb

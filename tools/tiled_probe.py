@@ -17,4 +17,4 @@ for rep in range(2):
     torch.cuda.synchronize(); t0 = time.time()
     bs = d.solve(c4.pixels, lam, cfg, backend, seeds=seeds)
     torch.cuda.synchronize(); dt = time.time() - t0
-    print(f"{backend} P={P} iters={iters}: {dt*1000:.1f} ms, {dt/iters*1000:.2f} ms/round, {P*iters*16*100*160000/(8 if backend=='rbpg' else 1)/dt/1e12:.2f} TF/s")
+    print(f"tc={os.environ.get('TB_TILED_TC','-')} F={float(bs.objective_final.double().sum()):.12e} {backend} P={P} iters={iters}: {dt*1000:.1f} ms, {dt/iters*1000:.2f} ms/round, {P*iters*16*100*160000/(8 if backend=='rbpg' else 1)/dt/1e12:.2f} TF/s")
