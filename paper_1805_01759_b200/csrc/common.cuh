@@ -30,6 +30,22 @@ __device__ __forceinline__ void cfma_conj(float2& acc, float2 a, float2 b) {
   acc.y = fmaf(a.x, b.y, acc.y);
   acc.y = fmaf(-a.y, b.x, acc.y);
 }
+// acc += conj(a) * r with r4 = (r.x, r.y, r.y, -r.x): two packed FFMA2 (a.x and a.y as scalar
+// broadcast operands), the same per-component rounding sequence as cfma_conj.
+__device__ __forceinline__ void cfma_conj_x2(float2& acc, float2 a, float4 r4) {
+  asm("{\n\t.reg .b64 c, aa, bb, r01, r23;\n\t"
+      "mov.b64 c, {%0, %1};\n\t"
+      "mov.b64 aa, {%2, %2};\n\t"
+      "mov.b64 bb, {%3, %3};\n\t"
+      "mov.b64 r01, {%4, %5};\n\t"
+      "mov.b64 r23, {%6, %7};\n\t"
+      "fma.rn.f32x2 c, aa, r01, c;\n\t"
+      "fma.rn.f32x2 c, bb, r23, c;\n\t"
+      "mov.b64 {%0, %1}, c;\n\t}"
+      : "+f"(acc.x), "+f"(acc.y)
+      : "f"(a.x), "f"(a.y), "f"(r4.x), "f"(r4.y), "f"(r4.z), "f"(r4.w));
+}
+__device__ __forceinline__ float4 conj_operand(float rx, float ry) { return make_float4(rx, ry, ry, -rx); }
 __device__ __forceinline__ float cabs2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
 __device__ __forceinline__ float cabsf(float2 a) { return sqrtf(fmaf(a.x, a.x, a.y * a.y)); }
 

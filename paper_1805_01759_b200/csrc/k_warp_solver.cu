@@ -71,9 +71,9 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp
   double2* apv = rv + n;                         // A x_prev (FISTA)
   double2* xs = apv + n;                         // x (fp64 iterate)
   double2* zs = xs + m;                          // broadcast buffer for forward products [max_width]
-  float2* ds = reinterpret_cast<float2*>(zs + P.max_width);  // d = x - prev, fp32 (y = x + m_k d)
-  float2* ryv = ds + m;                          // r_y rounded for the adjoint
-  float2* bv = ryv + n;                          // b
+  float4* ryv = reinterpret_cast<float4*>(zs + P.max_width);  // r_y rounded, as (r.x, r.y, r.y, -r.x)
+  float2* ds = reinterpret_cast<float2*>(ryv + n);  // d = x - prev, fp32 (y = x + m_k d)
+  float2* bv = ds + m;                           // b
   double* ring = reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
   double* l1blk = ring + 16;                     // RBPG: sum |x_b| per block (updated on accept)
 
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp
           if (i < n) {
             const double2 r = rv[i];
             ry[q] = any_dy ? make_double2(r.x + acc[q].x, r.y + acc[q].y) : r;
-            ryv[i] = make_float2((float)ry[q].x, (float)ry[q].y);
+            ryv[i] = conj_operand((float)ry[q].x, (float)ry[q].y);
           }
         }
       } else {
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp
             }
             ay[q] = a;
             ry[q] = make_double2(a.x - b.x, a.y - b.y);
-            ryv[i] = make_float2((float)ry[q].x, (float)ry[q].y);
+            ryv[i] = conj_operand((float)ry[q].x, (float)ry[q].y);
           }
         }
       }
@@ -251,10 +251,10 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp
         const int stride = ASMEM ? ms : m;
         int aoff = 0;
         for (int i = 0; i < n; ++i, aoff += stride) {
-          const float2 r = ryv[i];
+          const float4 r = ryv[i];
 #pragma unroll
           for (int t = 0; t < MAXT; ++t) {
-            if (lane + 32 * t < width) cfma_conj(acc[t], ASMEM ? acol[aoff + 32 * t] : __ldg(acol + aoff + 32 * t), r);
+            if (lane + 32 * t < width) cfma_conj_x2(acc[t], ASMEM ? acol[aoff + 32 * t] : __ldg(acol + aoff + 32 * t), r);
           }
         }
 #pragma unroll
