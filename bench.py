@@ -112,6 +112,17 @@ def fp32_peak():
         return 70.78, "tools/peak_probe.cu FFMA burst on B200 (70.78 TFLOP/s, round 1)"
 
 
+def ncu_traffic(key: str):
+    """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
+    (profiles/ncu_traffic.json, keyed workload/backend/pixels), or None when not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            e = json.load(fh)[key]
+        return float(e["dram_bytes_per_launch"]), e["source"]
+    except Exception:
+        return None, None
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -253,6 +264,7 @@ def run_b200(args):
     st = est.solution.status.cpu().numpy()
     its = est.solution.iterations.cpu().numpy()
 
+    traffic, traffic_src = ncu_traffic(f"cfg{args.config}/{args.backend}/{P}")
     line = None
     if rank == 0:
         line = {
@@ -267,7 +279,8 @@ def run_b200(args):
             },
             "roofline": {
                 "bound": "fp32", "kernel": "warp_solver_kernel", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu)", "traffic_source": traffic_src,
+                "peak_source": peak_src,
                 "algorithmic": f"{flop_pi:.0f} flop per pixel-iteration (16 n m{'/J' if args.backend == 'rbpg' else ''}) x {pix_iters / args.steps:.4g} pixel-iterations per launch",
                 "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms_per_step,
             },
