@@ -55,6 +55,27 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(TB_FULL_MASK, v, o);
   return v;
 }
+// Warp all-reduce of four doubles by recursive halving: at xor 16 and 8 each lane forwards the
+// half it does not keep, so 10 double shuffles (plus 4 broadcasts) replace 20.  Every lane ends
+// with the same four sums.
+__device__ __forceinline__ void warp_sum4(double v[4]) {
+  const int lane = threadIdx.x & 31;
+  const bool h16 = lane & 16, h8 = lane & 8;
+  double k0 = h16 ? v[2] : v[0], k1 = h16 ? v[3] : v[1];
+  const double s0 = h16 ? v[0] : v[2], s1 = h16 ? v[1] : v[3];
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  double kk = h8 ? k1 : k0;
+  kk += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+  // value q = 2 * h16 + h8 now sits in lanes 8q .. 8q + 7
+  v[0] = __shfl_sync(0xffffffffu, kk, 0);
+  v[1] = __shfl_sync(0xffffffffu, kk, 8);
+  v[2] = __shfl_sync(0xffffffffu, kk, 16);
+  v[3] = __shfl_sync(0xffffffffu, kk, 24);
+}
 __device__ __forceinline__ float warp_sumf(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(TB_FULL_MASK, v, o);

@@ -34,7 +34,7 @@
 namespace tb {
 
 template <bool RB, int MAXT, int MAXQ, bool ASMEM>
-__global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp_solver_kernel(const SolveParams P) {
+__global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) warp_solver_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp
     if (lane == 0) ring[0] = F;
     if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
     const uint64_t seed = RB ? P.seeds[p] : 0ull;
-    uint64_t* rbuf = reinterpret_cast<uint64_t*>(ring + 12);  // 4 buffered Philox outputs
+    uint64_t* rbuf = reinterpret_cast<uint64_t*>(l1blk + J);  // 32 buffered Philox outputs
     int status = STATUS_MAX_ITERS;
     int iters = 0;
     bool stopped = false;
@@ -151,20 +151,24 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp
       // ---- block choice (solver.py:283, 217-219): searchsorted(cdf, u, 'right')
       int blk = 0, cs = 0, ce = m;
       if (RB) {
-        // raw draw k-1 of Philox(key=[seed, 0]): counter (k-1)/4 + 1, output (k-1) % 4
-        const int w = (k - 1) & 3;
+        // raw draw k-1 of Philox(key=[seed, 0]): counter (k-1)/4 + 1, output (k-1) % 4.  Every 32
+        // draws, lanes 0..7 evaluate the next 8 counters in parallel into the slot's buffer.
+        const int w = (k - 1) & 31;
         if (w == 0) {
-          uint64_t c4[4] = {(uint64_t)((k - 1) >> 2) + 1ull, 0ull, 0ull, 0ull};
+          uint64_t c4[4] = {(uint64_t)((k - 1) >> 2) + 1ull + (uint64_t)(lane & 7), 0ull, 0ull, 0ull};
           philox4x64_10(c4, seed, 0ull);
-          if (lane < 4) rbuf[lane] = lane == 0 ? c4[0] : lane == 1 ? c4[1] : lane == 2 ? c4[2] : c4[3];
+          if (lane < 8) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rbuf[4 * lane + q] = c4[q];
+          }
           __syncwarp();
         }
         const double u = raw_to_unit(rbuf[w]);
         int j = 0;
-        if (J <= 8) {
-          // searchsorted(cdf, u, 'right') with cdf[J-1] == 1 > u: count of cdf[j] <= u, j < J-1
-#pragma unroll
-          for (int q = 0; q < 7; ++q) j += (q < J - 1 && s_cdf[q] <= u) ? 1 : 0;
+        if (J <= 32) {
+          // searchsorted(cdf, u, 'right') with cdf[J-1] == 1 > u: count of cdf[q] <= u over q < J-1
+          const bool le = lane < J - 1 && s_cdf[lane] <= u;
+          j = __popc(__ballot_sync(TB_FULL_MASK, le));
         } else {
           while (j < J - 1 && s_cdf[j] <= u) ++j;
         }
@@ -249,13 +253,25 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp
         for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
         const float2* acol = ASMEM ? As + cs + lane : P.A + cs + lane;
         const int stride = ASMEM ? ms : m;
-        int aoff = 0;
-        for (int i = 0; i < n; ++i, aoff += stride) {
+        // rows unrolled by 4 (loop and address overhead once per 4 rows)
+        int i = 0;
+        const float2* ap = acol;
+#pragma unroll 1
+        for (; i + 4 <= n; i += 4, ap += 4 * stride) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 r = ryv[i + u];
+#pragma unroll
+            for (int t = 0; t < MAXT; ++t)
+              if (lane + 32 * t < width) cfma_conj_x2(acc[t], ASMEM ? ap[u * stride + 32 * t] : __ldg(ap + u * stride + 32 * t), r);
+          }
+        }
+#pragma unroll 1
+        for (; i < n; ++i, ap += stride) {
           const float4 r = ryv[i];
 #pragma unroll
-          for (int t = 0; t < MAXT; ++t) {
-            if (lane + 32 * t < width) cfma_conj_x2(acc[t], ASMEM ? acol[aoff + 32 * t] : __ldg(acol + aoff + 32 * t), r);
-          }
+          for (int t = 0; t < MAXT; ++t)
+            if (lane + 32 * t < width) cfma_conj_x2(acc[t], ASMEM ? ap[32 * t] : __ldg(ap + 32 * t), r);
         }
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) g[t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
@@ -322,10 +338,14 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB) warp
             }
           }
         }
+        if (RB) {
+          warp_sum4(red);
+        } else {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+          for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-          for (int r = 0; r < (RB ? 4 : 5); ++r) red[r] += __shfl_xor_sync(TB_FULL_MASK, red[r], o);
+            for (int r = 0; r < 5; ++r) red[r] += __shfl_xor_sync(TB_FULL_MASK, red[r], o);
+          }
         }
         __syncwarp();
         l1z = red[1];
