@@ -112,6 +112,46 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       if (lane + 32 * q >= n) acc[q] = make_double2(0.0, 0.0);
   };
 
+  // RBPG variant: zs[0..cnt) holds the nonzero entries compacted in ascending column order with
+  // their block-local columns in clist (same accumulation order as `forward`), two per step.
+  auto forward_list = [&](int cs, const int* cl, int cnt, double2* acc) {
+    const float2* arow[MAXQ];
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      acc[q] = make_double2(0.0, 0.0);
+      const int i = min(lane + 32 * q, n - 1);
+      arow[q] = ASMEM ? As + i * ms + cs : P.A + (size_t)i * m + cs;
+    }
+    int e = 0;
+    for (; e + 2 <= cnt; e += 2) {
+      const int2 cc = *reinterpret_cast<const int2*>(cl + e);
+      const double2 v0 = zs[e], v1 = zs[e + 1];
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const float2 a0 = ASMEM ? arow[q][cc.x] : __ldg(arow[q] + cc.x);
+        const float2 a1 = ASMEM ? arow[q][cc.y] : __ldg(arow[q] + cc.y);
+        acc[q].x = fma((double)a0.x, v0.x, fma(-(double)a0.y, v0.y, acc[q].x));
+        acc[q].y = fma((double)a0.x, v0.y, fma((double)a0.y, v0.x, acc[q].y));
+        acc[q].x = fma((double)a1.x, v1.x, fma(-(double)a1.y, v1.y, acc[q].x));
+        acc[q].y = fma((double)a1.x, v1.y, fma((double)a1.y, v1.x, acc[q].y));
+      }
+    }
+    if (e < cnt) {
+      const int c = cl[e];
+      const double2 v = zs[e];
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const float2 a = ASMEM ? arow[q][c] : __ldg(arow[q] + c);
+        acc[q].x = fma((double)a.x, v.x, fma(-(double)a.y, v.y, acc[q].x));
+        acc[q].y = fma((double)a.x, v.y, fma((double)a.y, v.x, acc[q].y));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q)
+      if (lane + 32 * q >= n) acc[q] = make_double2(0.0, 0.0);
+  };
+  const unsigned lt_mask = (1u << lane) - 1u;
+
   for (;;) {
     unsigned long long pq = 0;
     if (lane == 0) pq = atomicAdd(P.queue, 1ull);
@@ -141,6 +181,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
     const uint64_t seed = RB ? P.seeds[p] : 0ull;
     uint64_t* rbuf = reinterpret_cast<uint64_t*>(l1blk + J);  // 32 buffered Philox outputs
+    int* clist = reinterpret_cast<int*>(rbuf + 32);               // RBPG: nonzero columns of zs, ascending
     int status = STATUS_MAX_ITERS;
     int iters = 0;
     bool stopped = false;
@@ -184,10 +225,12 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       double2 z[RB ? MAXT : 1];
       unsigned masks[MAXT];
       bool any_dy = false;
+      int cnt = 0;  // RBPG: compacted nonzero count in zs / clist
 #pragma unroll
       for (int t = 0; t < MAXT; ++t) {
         const int cl = lane + 32 * t;
         bool nz = false;
+        double2 dyv = make_double2(0.0, 0.0);
         if (cl < width) {
           const double2 xv = xs[cs + cl];
           double2 yv = xv;
@@ -199,12 +242,17 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
             yv.y = fma(mk, (double)dv.y, xv.y);
           }
           if (RB) {
-            const double2 dy = make_double2(yv.x - xv.x, yv.y - xv.y);
-            zs[cl] = dy;
-            nz = (dy.x != 0.0) || (dy.y != 0.0);
+            dyv = make_double2(yv.x - xv.x, yv.y - xv.y);
+            nz = (dyv.x != 0.0) || (dyv.y != 0.0);
           }
         }
         masks[t] = __ballot_sync(TB_FULL_MASK, nz);
+        if (RB && nz) {
+          const int pos = cnt + __popc(masks[t] & lt_mask);
+          zs[pos] = dyv;
+          clist[pos] = cl;
+        }
+        cnt += __popc(masks[t]);
         any_dy |= masks[t] != 0u;
       }
       __syncwarp();
@@ -214,7 +262,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       double2 ry[MAXQ], ay[MAXQ];
       if (RB) {
         double2 acc[MAXQ];
-        if (any_dy) forward(cs, masks, acc);
+        if (any_dy) forward_list(cs, clist, cnt, acc);
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
           const int i = lane + 32 * q;
@@ -286,10 +334,12 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         const double tau = alpha * lamd;
         const double tau2 = tau * tau;
         double red[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // |d|^2, |z|, ||A d||^2, f(z), scale (FISTA)
+        cnt = 0;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
           const int cl = lane + 32 * t;
           bool nz = false;
+          double2 dw = make_double2(0.0, 0.0);
           if (cl < width) {
             // y = x + m_k d recomputed from shared memory (keeps registers for occupancy)
             const double2 xv = xs[cs + cl];
@@ -312,13 +362,23 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
             const double2 d = make_double2(zz.x - yv.x, zz.y - yv.y);
             red[0] += fma(d.x, d.x, d.y * d.y);
             const double2 w = RB ? d : zz;
-            zs[cl] = w;
+            if (!RB) zs[cl] = w;
             nz = (w.x != 0.0) || (w.y != 0.0);
+            if (RB) dw = d;
           }
           masks[t] = __ballot_sync(TB_FULL_MASK, nz);
+          if (RB && nz) {
+            const int pos = cnt + __popc(masks[t] & lt_mask);
+            zs[pos] = dw;
+            clist[pos] = cl;
+          }
+          if (RB) cnt += __popc(masks[t]);
         }
         __syncwarp();
-        forward(cs, masks, adz);  // RBPG: A_b dz; FISTA/ISTA: A z
+        if (RB)
+          forward_list(cs, clist, cnt, adz);  // A_b dz
+        else
+          forward(cs, masks, adz);  // FISTA/ISTA: A z
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
           const int i = lane + 32 * q;

@@ -39,9 +39,9 @@ struct SolveParams {
 
 // per-warp shared bytes: 2 fp64 n-vectors, fp64 x (m) + fp64 broadcast buffer (width), fp32 d = x - prev
 // (m), fp32 r_y as float4 + fp32 b (n each), 16-double ring, J-double per-block l1 cache, 32 buffered
-// Philox outputs
+// Philox outputs, width ints (compacted nonzero columns)
 __host__ __device__ inline size_t warp_slot_bytes(int n, int m, int width, int J) {
-  size_t b = (size_t)n * 32 + (size_t)(m + width) * 16 + (size_t)m * 8 + (size_t)n * 24 + 16 * 8 + (size_t)J * 8 + 32 * 8;
+  size_t b = (size_t)n * 32 + (size_t)(m + width) * 16 + (size_t)m * 8 + (size_t)n * 24 + 16 * 8 + (size_t)J * 8 + 32 * 8 + (size_t)width * 4;
   return (b + 15) & ~(size_t)15;
 }
 // per-CTA block tables: cdf, alpha0 (J doubles each) + J+1 block starts
