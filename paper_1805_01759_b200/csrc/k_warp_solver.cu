@@ -81,39 +81,10 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     if (ASMEM) return As[(size_t)i * ms + c];
     return __ldg(&P.A[(size_t)i * m + c]);
   };
-  // acc[q] += sum over the nonzero entries of zs (bitmask per 32-column chunk, built with
-  // __ballot_sync) of A[i][cs + c] * zs[c], fp64 accumulation.  L1 iterates and their steps are
-  // sparse, so only the few surviving columns are visited (warp-uniform loop).
-  auto forward = [&](int cs, const unsigned* masks, double2* acc) {
-    const float2* arow[MAXQ];
-#pragma unroll
-    for (int q = 0; q < MAXQ; ++q) {
-      acc[q] = make_double2(0.0, 0.0);
-      const int i = min(lane + 32 * q, n - 1);
-      arow[q] = ASMEM ? As + i * ms + cs : P.A + (size_t)i * m + cs;
-    }
-#pragma unroll
-    for (int t = 0; t < MAXT; ++t) {
-      unsigned mk = masks[t];
-      while (mk) {
-        const int c = (__ffs(mk) - 1) + 32 * t;
-        mk &= mk - 1;
-        const double2 v = zs[c];
-#pragma unroll
-        for (int q = 0; q < MAXQ; ++q) {
-          const float2 a = ASMEM ? arow[q][c] : __ldg(arow[q] + c);
-          acc[q].x = fma((double)a.x, v.x, fma(-(double)a.y, v.y, acc[q].x));
-          acc[q].y = fma((double)a.x, v.y, fma((double)a.y, v.x, acc[q].y));
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < MAXQ; ++q)
-      if (lane + 32 * q >= n) acc[q] = make_double2(0.0, 0.0);
-  };
-
-  // RBPG variant: zs[0..cnt) holds the nonzero entries compacted in ascending column order with
-  // their block-local columns in clist (same accumulation order as `forward`), two per step.
+  // acc[q] += sum over the nonzero entries of the step (lane = row), fp64 accumulation.  L1 iterates
+  // and their steps are sparse: the lanes compact the nonzero entries with __ballot_sync into
+  // zs[0..cnt) in ascending column order, their block-local columns in clist, and only those
+  // columns are visited, two per step (warp-uniform loop).
   auto forward_list = [&](int cs, const int* cl, int cnt, double2* acc) {
     const float2* arow[MAXQ];
 #pragma unroll
@@ -181,7 +152,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
     const uint64_t seed = RB ? P.seeds[p] : 0ull;
     uint64_t* rbuf = reinterpret_cast<uint64_t*>(l1blk + J);  // 32 buffered Philox outputs
-    int* clist = reinterpret_cast<int*>(rbuf + 32);               // RBPG: nonzero columns of zs, ascending
+    int* clist = reinterpret_cast<int*>(rbuf + 32);               // nonzero columns of zs, ascending
     int status = STATUS_MAX_ITERS;
     int iters = 0;
     bool stopped = false;
@@ -361,24 +332,19 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
             if (RB) z[t] = zz;
             const double2 d = make_double2(zz.x - yv.x, zz.y - yv.y);
             red[0] += fma(d.x, d.x, d.y * d.y);
-            const double2 w = RB ? d : zz;
-            if (!RB) zs[cl] = w;
-            nz = (w.x != 0.0) || (w.y != 0.0);
-            if (RB) dw = d;
+            dw = RB ? d : zz;
+            nz = (dw.x != 0.0) || (dw.y != 0.0);
           }
           masks[t] = __ballot_sync(TB_FULL_MASK, nz);
-          if (RB && nz) {
+          if (nz) {
             const int pos = cnt + __popc(masks[t] & lt_mask);
             zs[pos] = dw;
             clist[pos] = cl;
           }
-          if (RB) cnt += __popc(masks[t]);
+          cnt += __popc(masks[t]);
         }
         __syncwarp();
-        if (RB)
-          forward_list(cs, clist, cnt, adz);  // A_b dz
-        else
-          forward(cs, masks, adz);  // FISTA/ISTA: A z
+        forward_list(cs, clist, cnt, adz);  // RBPG: A_b dz; FISTA/ISTA: A z
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
           const int i = lane + 32 * q;
@@ -467,14 +433,18 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         }
       } else {
         // x_prev <- x, x <- z, F = ||A z - b||^2 + lambda ||z||_1 (solver.py:362-364)
+        // z is nonzero only on the compacted list: the owner lane finds its entry from the masks
+        int base = 0;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
           const int cl = lane + 32 * t;
           if (cl < width) {
-            const double2 xv = xs[cl], zv = zs[cl];
+            const double2 xv = xs[cl];
+            const double2 zv = (masks[t] >> lane) & 1u ? zs[base + __popc(masks[t] & lt_mask)] : make_double2(0.0, 0.0);
             ds[cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
             xs[cl] = zv;
           }
+          base += __popc(masks[t]);
         }
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
