@@ -143,7 +143,7 @@ __host__ __device__ inline size_t tiled_pass_smem(int n) {
   b += (size_t)n * TL_AS * 8;                     // sA
   b = (b + 15) & ~(size_t)15;
   b += (size_t)TL_CT * TL_ZS * 16;                // sZ
-  b += TL_CT * 4;                                 // sFlag
+  b += TL_PT * 8;                                 // sMask
   b += TL_PT * (4 * 8 + 4 * 4);                   // per-pixel scalars
   return (b + 15) & ~(size_t)15;
 }
@@ -165,8 +165,8 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
   float2* sA = sRY + (size_t)n * TL_PT;         // [n][TL_AS]
   size_t o = ((size_t)n * TL_PT * 8 + (size_t)n * TL_AS * 8 + 15) & ~(size_t)15;
   double2* sZ = reinterpret_cast<double2*>(sm + o);  // [CT][ZS]
-  int* sFlag = reinterpret_cast<int*>(sZ + TL_CT * TL_ZS);
-  double* sAlpha = reinterpret_cast<double*>(sFlag + TL_CT);
+  unsigned long long* sMask = reinterpret_cast<unsigned long long*>(sZ + TL_CT * TL_ZS);  // [PT] nonzero columns
+  double* sAlpha = reinterpret_cast<double*>(sMask + TL_PT);
   double* sTau = sAlpha + TL_PT;
   double* sMk = sTau + TL_PT;
   double* sPad = sMk + TL_PT;
@@ -216,7 +216,6 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
       const int i = idx / TL_CT, c = idx - i * TL_CT;
       sA[i * TL_AS + c] = c < ncols ? __ldg(&T.A[(size_t)i * m + col0 + c]) : make_float2(0.f, 0.f);
     }
-    if (tid < TL_CT) sFlag[tid] = 0;
     __syncthreads();
 
     // ---- adjoint: g = 2 A^H r_y for pixels (2pg, 2pg+1), columns cg + 16 j
@@ -251,6 +250,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
     for (int q = 0; q < 2; ++q) {
       const int slot = 2 * pg + q;
       const int p = sPid[slot];
+      unsigned long long nzm = 0ull;  // this half-warp's pixel: nonzero columns of the tile
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int c = cg + 16 * j;
@@ -279,22 +279,61 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
           sd2[q] += fma(d.x, d.x, d.y * d.y);
           sy2[q] += fma(y.x, y.x, y.y * y.y);
           w = rb ? d : z;
-          if (w.x != 0.0 || w.y != 0.0) sFlag[c] = 1;
         }
         sZ[c * TL_ZS + slot] = w;
+        // lanes 0-15 hold pixel slot 2*(2*warp)+q, lanes 16-31 slot 2*(2*warp+1)+q, columns cg + 16 j
+        const unsigned bits = __ballot_sync(TB_FULL_MASK, w.x != 0.0 || w.y != 0.0);
+        nzm |= (unsigned long long)((lane < 16 ? bits : bits >> 16) & 0xFFFFu) << (16 * j);
       }
+      if (cg == 0) sMask[slot] = nzm;
     }
     __syncthreads();
-    // ---- forward partial over the tile's nonzero columns, fp64 (lane = row, 16 pixels)
-    for (int c = 0; c < ncols; ++c) {
-      if (!sFlag[c]) continue;
-      const float2 af = frow < n ? sA[frow * TL_AS + c] : make_float2(0.f, 0.f);
-      const double ax = af.x, ayv = af.y;
+    // ---- forward partial, fp64 (lane = row, 16 pixels per thread).  Dense over the union of the
+    //      16 pixels' nonzero columns (16 independent accumulator chains per column), or, when under
+    //      a quarter of that union x 16 block is nonzero (late, sparse iterates), per pixel over its
+    //      own nonzero columns.  Either way each pixel accumulates its columns in ascending order.
+    {
+      unsigned long long uni = 0ull;
+      int nnz = 0;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        const double2 z = sZ[c * TL_ZS + fph + q];
-        facc[q].x = fma(ax, z.x, fma(-ayv, z.y, facc[q].x));
-        facc[q].y = fma(ax, z.y, fma(ayv, z.x, facc[q].y));
+        const unsigned long long mq = sMask[fph + q];
+        uni |= mq;
+        nnz += __popcll(mq);
+      }
+      if (4 * nnz >= 16 * __popcll(uni)) {
+        while (uni) {
+          const int c = __ffsll((long long)uni) - 1;
+          uni &= uni - 1;
+          const float2 af = frow < n ? sA[frow * TL_AS + c] : make_float2(0.f, 0.f);
+          const double ax = af.x, ayv = af.y;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const double2 z = sZ[c * TL_ZS + fph + q];
+            facc[q].x = fma(ax, z.x, fma(-ayv, z.y, facc[q].x));
+            facc[q].y = fma(ax, z.y, fma(ayv, z.x, facc[q].y));
+          }
+        }
+      } else {
+        // two pixels' chains interleaved for ILP (warp-uniform branches)
+        auto step = [&](unsigned long long& mq, double2& acc, int q) {
+          const int c = __ffsll((long long)mq) - 1;
+          mq &= mq - 1;
+          const float2 af = frow < n ? sA[frow * TL_AS + c] : make_float2(0.f, 0.f);
+          const double2 z = sZ[c * TL_ZS + fph + q];
+          acc.x = fma((double)af.x, z.x, fma(-(double)af.y, z.y, acc.x));
+          acc.y = fma((double)af.x, z.y, fma((double)af.y, z.x, acc.y));
+        };
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+          unsigned long long m0 = sMask[fph + q], m1 = sMask[fph + q + 1];
+          while (m0 && m1) {
+            step(m0, facc[q], q);
+            step(m1, facc[q + 1], q + 1);
+          }
+          while (m0) step(m0, facc[q], q);
+          while (m1) step(m1, facc[q + 1], q + 1);
+        }
       }
     }
   }

@@ -83,15 +83,15 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
   };
   // acc[q] += sum over the nonzero entries of the step (lane = row), fp64 accumulation.  L1 iterates
   // and their steps are sparse: the lanes compact the nonzero entries with __ballot_sync into
-  // zs[0..cnt) in ascending column order, their block-local columns in clist, and only those
+  // zs[0..cnt) in ascending column order, their dictionary columns in clist, and only those
   // columns are visited, two per step (warp-uniform loop).
-  auto forward_list = [&](int cs, const int* cl, int cnt, double2* acc) {
+  auto forward_list = [&](const int* cl, int cnt, double2* acc) {
     const float2* arow[MAXQ];
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
       acc[q] = make_double2(0.0, 0.0);
       const int i = min(lane + 32 * q, n - 1);
-      arow[q] = ASMEM ? As + i * ms + cs : P.A + (size_t)i * m + cs;
+      arow[q] = ASMEM ? As + i * ms : P.A + (size_t)i * m;
     }
     int e = 0;
     for (; e + 2 <= cnt; e += 2) {
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         if (RB && nz) {
           const int pos = cnt + __popc(masks[t] & lt_mask);
           zs[pos] = dyv;
-          clist[pos] = cl;
+          clist[pos] = cs + cl;
         }
         cnt += __popc(masks[t]);
         any_dy |= masks[t] != 0u;
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       double2 ry[MAXQ], ay[MAXQ];
       if (RB) {
         double2 acc[MAXQ];
-        if (any_dy) forward_list(cs, clist, cnt, acc);
+        if (any_dy) forward_list(clist, cnt, acc);
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
           const int i = lane + 32 * q;
@@ -272,13 +272,13 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
         const float2* acol = ASMEM ? As + cs + lane : P.A + cs + lane;
         const int stride = ASMEM ? ms : m;
-        // rows unrolled by 4 (loop and address overhead once per 4 rows)
+        // rows unrolled by 8 (loop and address overhead once per 8 rows)
         int i = 0;
         const float2* ap = acol;
 #pragma unroll 1
-        for (; i + 4 <= n; i += 4, ap += 4 * stride) {
+        for (; i + 8 <= n; i += 8, ap += 8 * stride) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < 8; ++u) {
             const float4 r = ryv[i + u];
 #pragma unroll
             for (int t = 0; t < MAXT; ++t)
@@ -339,12 +339,12 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           if (nz) {
             const int pos = cnt + __popc(masks[t] & lt_mask);
             zs[pos] = dw;
-            clist[pos] = cl;
+            clist[pos] = cs + cl;
           }
           cnt += __popc(masks[t]);
         }
         __syncwarp();
-        forward_list(cs, clist, cnt, adz);  // RBPG: A_b dz; FISTA/ISTA: A z
+        forward_list(clist, cnt, adz);  // RBPG: A_b dz; FISTA/ISTA: A z
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) {
           const int i = lane + 32 * q;

@@ -31,6 +31,11 @@ struct tb_ctx {
   int mk_len = 0;
   std::vector<double> lip_host;  // per-block Lipschitz (host copy)
   std::vector<int> bstart_host;  // J+1
+  // tiled-solver workspace, grow-only and kept across solves: re-allocating tens of GB per call
+  // costs page mapping time on every solve (one tiled handle per context at a time)
+  unsigned char* ws = nullptr;
+  size_t ws_size = 0;
+  bool ws_busy = false;
 };
 
 struct tb_tiled {
@@ -133,6 +138,7 @@ int tb_ctx_destroy(tb_ctx* c) {
   cudaFree(c->cdf);
   cudaFree(c->queue);
   cudaFree(c->mk);
+  cudaFree(c->ws);
   delete c;
   return TB_OK;
 }
@@ -386,14 +392,22 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   sz[ns++] = tc ? align256(sizeof(int) * (J + 1)) : 0;                                   // tile_base
   size_t tot = 0;
   for (int i = 0; i < ns; ++i) tot += sz[i];
-  size_t fr = 0, tt = 0;
-  cudaMemGetInfo(&fr, &tt);
-  if (tot > fr) return fail(TB_ERR_CAPACITY, "tiled solver needs %.1f GB for %lld pixels, %.1f GB free", tot / 1e9, (long long)P, fr / 1e9);
-  unsigned char* base = nullptr;
-  TB_CUDA(cudaMallocAsync((void**)&base, tot, st));
+  if (c->ws_busy) return fail(TB_ERR_INVALID, "one tiled solve per context at a time");
+  if (c->ws_size < tot) {
+    TB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(c->ws);
+    c->ws = nullptr;
+    c->ws_size = 0;
+    size_t fr = 0, tt = 0;
+    cudaMemGetInfo(&fr, &tt);
+    if (tot > fr) return fail(TB_ERR_CAPACITY, "tiled solver needs %.1f GB for %lld pixels, %.1f GB free", tot / 1e9, (long long)P, fr / 1e9);
+    TB_CUDA(cudaMalloc((void**)&c->ws, tot));
+    c->ws_size = tot;
+  }
+  unsigned char* base = c->ws;
   tb_tiled* h = new tb_tiled();
   h->ctx = c;
-  h->owned = base;
+  h->owned = nullptr;
   h->own_red = red_dev == nullptr;
   h->max_width = maxw;
   tb::TiledParams& T = h->T;
@@ -497,6 +511,7 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   TB_CUDA(cudaMemcpyAsync(T.remaining, &rem, sizeof(int), cudaMemcpyHostToDevice, st));
   TB_CUDA(tb::tiled_init(T, st));
   TB_CUDA(cudaStreamSynchronize(st));
+  c->ws_busy = true;
   *out = h;
   return TB_OK;
 }
@@ -547,7 +562,7 @@ int tb_tiled_destroy(tb_tiled* h) {
   if (!h) return TB_OK;
   cudaSetDevice(h->ctx->device);
   cudaDeviceSynchronize();
-  cudaFree(h->owned);
+  h->ctx->ws_busy = false;  // the workspace stays with the context
   delete h;
   return TB_OK;
 }
@@ -558,6 +573,7 @@ static int solve_tiled(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, c
   // pixel chunks sized to the free HBM (state is 3 fp64 copies of x per pixel)
   size_t fr = 0, tt = 0;
   TB_CUDA(cudaMemGetInfo(&fr, &tt));
+  fr += c->ws_size;  // the cached tiled workspace is reusable
   const double per_px = (tiled_use_tc() ? 56.0 : 48.0) * (double)c->m + 64.0 * c->n * (solver == TB_SOLVER_RBPG ? c->num_blocks + 4 : 5) + 4096;
   long long chunk = (long long)(0.6 * (double)fr / per_px);
   if (chunk < 1) return fail(TB_ERR_CAPACITY, "not enough device memory for one pixel of m = %lld", (long long)c->m);
