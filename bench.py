@@ -85,6 +85,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
             )
+            time.sleep(0.5)  # let nvidia-smi start up before the timed region (its start-up competes with launches)
         except Exception:
             self.proc = None
 
