@@ -58,6 +58,14 @@ def flops_per_pixel_iteration(backend, n, m, num_blocks):
     return 16.0 * n * m / (num_blocks if backend == "rbpg" else 1)
 
 
+class _Rows:
+    """A view of a synthetic batch restricted to the given pixel rows (CPU baseline sample)."""
+
+    def __init__(self, batch, idx):
+        self.dictionary = batch.dictionary
+        self.pixels = batch.pixels[idx]
+
+
 def cpu_baseline(batch, backend, sample, lam, seeds, workers, solver_kw):
     """The reference algorithm (oracle port, per-solve power iterations as in solver.py:267/344)."""
     from oracle import batch as OB
@@ -132,7 +140,7 @@ def run_reference(args):
     from oracle import tomo_oracle as O
 
     cores = os.cpu_count() or 1
-    sample = args.cpu_sample or max(cores * 24, 64)
+    sample = args.cpu_sample or (max(cores * 96, 64) if args.config <= 3 else cores)
     batch = make_config(args.config, num_pixels=sample)
     lam = lambda_from_beta(batch.dictionary, batch.pixels, 0.1)
     seeds = np.array([O.derive_seed(2018, p) for p in range(sample)], dtype=np.uint64)
@@ -295,22 +303,33 @@ def run_b200(args):
             from paper_1805_01759_b200.synth import lambda_from_beta
 
             cores = os.cpu_count() or 1
-            # bounded sample (~10-70 s of CPU work).  cfg1-3: whole solves of the first pixels.  cfg4: a
-            # full reference solve is ~0.2-1 h per pixel on one core, so one pixel per core runs a fixed
-            # 10 iterations (plus its per-solve power iterations) and the rate is scaled by the GPU
-            # run's mean iteration count - which overstates the CPU (setup amortised over 10, not ~300).
-            per_core = {1: 32, 2: 32, 3: 16}.get(args.config, 1)
-            sample = args.cpu_sample or max(cores * per_core, 16 if args.config <= 3 else cores)
-            lam_h = lambda_from_beta(batch.dictionary, batch.pixels[:sample], 0.1)
-            seeds_h = np.array([O.derive_seed(2018, p) for p in range(sample)], dtype=np.uint64)
             if args.config >= 4:
+                # a full reference solve is ~0.2-1 h per pixel on one core: one pixel per core runs a
+                # fixed 10 iterations (plus its per-solve power iterations) and the rate is scaled by
+                # the GPU run's mean iteration count - which overstates the CPU (setup amortised over 10).
                 fixed = 10
-                v, wall, _ = cpu_baseline(batch, args.backend, sample, lam_h, seeds_h, cores, dict(fixed_iters=fixed, tol=1e-6, num_blocks=8))
+                sample = args.cpu_sample or cores
+                idx = np.arange(sample) % P
+                lam_h = lambda_from_beta(batch.dictionary, batch.pixels[idx], 0.1)
+                seeds_h = np.array([O.derive_seed(2018, int(p)) for p in idx], dtype=np.uint64)
+                v, wall, _ = cpu_baseline(_Rows(batch, idx), args.backend, sample, lam_h, seeds_h, cores, dict(fixed_iters=fixed, tol=1e-6, num_blocks=8))
                 v *= fixed / max(float(its.mean()), 1.0)
-                what = f"first {sample} pixels of cfg{args.config}, {args.backend}, {fixed} fixed iterations each (+ per-solve power iterations), rate scaled by {fixed}/{float(its.mean()):.0f} (GPU mean iterations)"
+                what = f"{sample} pixels of cfg{args.config}, {args.backend}, {fixed} fixed iterations each (+ per-solve power iterations), rate scaled by {fixed}/{float(its.mean()):.0f} (GPU mean iterations)"
             else:
-                v, wall, _ = cpu_baseline(batch, args.backend, sample, lam_h, seeds_h, cores, dict(max_iters=500, tol=1e-6, num_blocks=8))
-                what = f"first {sample} pixels of cfg{args.config}, {args.backend}, whole solves"
+                # whole solves (max_iters=500, tol=1e-6) of the first pixels, cycling over the batch.
+                # A short calibration pass sizes the timed sample to ~12 s of wall time on all cores.
+                kw = dict(max_iters=500, tol=1e-6, num_blocks=8)
+
+                def timed(count):
+                    idx = np.arange(count) % P
+                    lam_h = lambda_from_beta(batch.dictionary, batch.pixels[idx], 0.1)
+                    seeds_h = np.array([O.derive_seed(2018, int(p)) for p in idx], dtype=np.uint64)
+                    return cpu_baseline(_Rows(batch, idx), args.backend, count, lam_h, seeds_h, cores, kw)
+
+                rate, _, _ = timed(cores * 4)
+                sample = args.cpu_sample or int(min(max(rate * 12.0, cores * 8), 200_000))
+                v, wall, _ = timed(sample)
+                what = f"{sample} pixels of cfg{args.config} (ids 0.. cycling over the batch), {args.backend}, whole solves"
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": f"{what}, process pool x{cores}, {wall:.1f} s wall, per-solve power iterations as solver.py:267/344"}
     if world > 1:
         dist.barrier()

@@ -24,6 +24,9 @@
 #include "common.cuh"
 #include "solver_params.h"
 
+#ifndef TB_WS_RSQRT
+#define TB_WS_RSQRT 1  // soft threshold from one fp64 rsqrt
+#endif
 #ifndef TB_WARP_LB_WIDE
 #define TB_WARP_LB_WIDE 384
 #endif
@@ -32,6 +35,42 @@
 #endif
 
 namespace tb {
+
+// acc[t] += conj(A[i][c + 32 t]) r_y[i] over all n rows for NP column passes (lane = column; only the
+// last pass can be partial: `last` = lane + 32 (NP - 1) < width), rows unrolled by 8 (loop and
+// address overhead once per 8 rows), fp32 packed FFMA2 sharing each broadcast r_y load.
+template <int NP, bool ASMEM>
+__device__ __forceinline__ void adjoint_passes(float2* acc, const float2* ap, int stride, const float4* ryv, int n, bool last) {
+  int i = 0;
+#pragma unroll 1
+  for (; i + 8 <= n; i += 8, ap += 8 * stride) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float4 r = ryv[i + u];
+#pragma unroll
+      for (int t = 0; t < NP; ++t)
+        if (t < NP - 1 || last) cfma_conj_x2(acc[t], ASMEM ? ap[u * stride + 32 * t] : __ldg(ap + u * stride + 32 * t), r);
+    }
+  }
+#pragma unroll 1
+  for (; i < n; ++i, ap += stride) {
+    const float4 r = ryv[i];
+#pragma unroll
+    for (int t = 0; t < NP; ++t)
+      if (t < NP - 1 || last) cfma_conj_x2(acc[t], ASMEM ? ap[32 * t] : __ldg(ap + 32 * t), r);
+  }
+}
+// runtime pass count -> compile-time unrolled body (no all-idle passes are issued)
+template <int NP, int MAXT, bool ASMEM>
+__device__ __forceinline__ void adjoint_dispatch(int passes, float2* acc, const float2* ap, int stride, const float4* ryv, int n, bool last) {
+  if constexpr (NP <= MAXT) {
+    if (passes == NP) {
+      adjoint_passes<NP, ASMEM>(acc, ap, stride, ryv, n, last);
+      return;
+    }
+    adjoint_dispatch<NP + 1, MAXT, ASMEM>(passes, acc, ap, stride, ryv, n, last);
+  }
+}
 
 template <bool RB, int MAXT, int MAXQ, bool ASMEM>
 __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) warp_solver_kernel(const SolveParams P) {
@@ -149,6 +188,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     if (RB)
       for (int j = lane; j < J; j += 32) l1blk[j] = 0.0;
     if (lane == 0) ring[0] = F;
+    int ridx = 0;  // k mod (STOP_WINDOW + 1), kept incrementally
     if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
     const uint64_t seed = RB ? P.seeds[p] : 0ull;
     uint64_t* rbuf = reinterpret_cast<uint64_t*>(l1blk + J);  // 32 buffered Philox outputs
@@ -160,6 +200,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
 
     for (int k = 1; k <= P.total_iters; ++k) {
       iters = k;
+      ridx = ridx == STOP_WINDOW ? 0 : ridx + 1;
       // ---- block choice (solver.py:283, 217-219): searchsorted(cdf, u, 'right')
       int blk = 0, cs = 0, ce = m;
       if (RB) {
@@ -265,33 +306,14 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       }
       __syncwarp();
 
-      // ---- block gradient g = 2 A_b^H r_y (solver.py:293, prox.py:77-79), fp32 products
+      // ---- block gradient g = 2 A_b^H r_y (solver.py:293, prox.py:77-79), fp32 products;
+      //      exactly ceil(width / 32) column passes are issued
       {
         float2 acc[MAXT];
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
-        const float2* acol = ASMEM ? As + cs + lane : P.A + cs + lane;
-        const int stride = ASMEM ? ms : m;
-        // rows unrolled by 8 (loop and address overhead once per 8 rows)
-        int i = 0;
-        const float2* ap = acol;
-#pragma unroll 1
-        for (; i + 8 <= n; i += 8, ap += 8 * stride) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const float4 r = ryv[i + u];
-#pragma unroll
-            for (int t = 0; t < MAXT; ++t)
-              if (lane + 32 * t < width) cfma_conj_x2(acc[t], ASMEM ? ap[u * stride + 32 * t] : __ldg(ap + u * stride + 32 * t), r);
-          }
-        }
-#pragma unroll 1
-        for (; i < n; ++i, ap += stride) {
-          const float4 r = ryv[i];
-#pragma unroll
-          for (int t = 0; t < MAXT; ++t)
-            if (lane + 32 * t < width) cfma_conj_x2(acc[t], ASMEM ? ap[32 * t] : __ldg(ap + 32 * t), r);
-        }
+        const int passes = (width + 31) >> 5;
+        adjoint_dispatch<1, MAXT, ASMEM>(passes, acc, (ASMEM ? As : P.A) + cs + lane, ASMEM ? ms : m, ryv, n, lane + 32 * (passes - 1) < width);
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) g[t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
       }
@@ -324,10 +346,18 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
             const double mag2 = fma(v.x, v.x, v.y * v.y);
             double2 zz = make_double2(0.0, 0.0);
             if (mag2 > tau2) {  // soft_threshold: zero iff |v| <= tau (prox.py:82-96)
+              // scale 1 - tau/|v| and |z| = |v| - tau from one fp64 reciprocal square root
+#if TB_WS_RSQRT
+              const double rs = rsqrt(mag2);
+              const double sc = fma(-tau, rs, 1.0);
+              zz = make_double2(v.x * sc, v.y * sc);
+              red[1] += fma(mag2, rs, -tau);
+#else
               const double mag = sqrt(mag2);
               const double sc = 1.0 - tau / mag;
               zz = make_double2(v.x * sc, v.y * sc);
               red[1] += mag * sc;
+#endif
             }
             if (RB) z[t] = zz;
             const double2 d = make_double2(zz.x - yv.x, zz.y - yv.y);
@@ -391,7 +421,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       if (!ok) {
         // RBPG appends F before breaking (solver.py:311-314); ISTA/FISTA do not (solver.py:357-361)
         if (RB) {
-          if (lane == 0) ring[k % (STOP_WINDOW + 1)] = F;
+          if (lane == 0) ring[ridx] = F;
           if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride + k] = F;
         }
         status = STATUS_LINE_SEARCH_FAILURE;
@@ -457,7 +487,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         F = fzs + lamd * l1z;
       }
       // ---- history, failure and window stop (solver.py:326-336, 366-374)
-      if (lane == 0) ring[k % (STOP_WINDOW + 1)] = F;
+      if (lane == 0) ring[ridx] = F;
       if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride + k] = F;
       __syncwarp();
       if (!isfinite(F)) {
@@ -466,7 +496,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         break;
       }
       if (!P.fixed && k >= STOP_WINDOW) {
-        const double ref = ring[(k - STOP_WINDOW) % (STOP_WINDOW + 1)];
+        const double ref = ring[ridx == STOP_WINDOW ? 0 : ridx + 1];  // F at k - STOP_WINDOW
         if (fabs(F - ref) <= P.tol * fmax(fabs(ref), 1e-300)) {
           status = STATUS_CONVERGED;
           stopped = true;
@@ -475,7 +505,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       }
     }
     if (!stopped && iters >= STOP_WINDOW) {  // for-else re-check (solver.py:334-336)
-      const double ref = ring[(iters - STOP_WINDOW) % (STOP_WINDOW + 1)];
+      const double ref = ring[ridx == STOP_WINDOW ? 0 : ridx + 1];
       if (fabs(F - ref) <= P.tol * fmax(fabs(ref), 1e-300)) status = STATUS_CONVERGED;
     }
     __syncwarp();
@@ -516,6 +546,7 @@ static cudaError_t launch_tq(const SolveParams& P, int maxt, int maxq, int warps
   if (maxt <= 2) return launch_q<RB, 2, ASMEM>(P, maxq, warps, smem, grid, st);
   if (maxt <= 4) return launch_q<RB, 4, ASMEM>(P, maxq, warps, smem, grid, st);
   if (maxt <= 8) return launch_q<RB, 8, ASMEM>(P, maxq, warps, smem, grid, st);
+  if (maxt <= 12) return launch_q<RB, 12, ASMEM>(P, maxq, warps, smem, grid, st);
   if (maxt <= 16) return launch_q<RB, 16, ASMEM>(P, maxq, warps, smem, grid, st);
   return cudaErrorInvalidValue;
 }
@@ -524,7 +555,7 @@ static cudaError_t launch_tq(const SolveParams& P, int maxt, int maxq, int warps
 cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps) {
   const int width = P.max_width;
   int maxt = (width + 31) / 32;
-  maxt = maxt <= 2 ? 2 : maxt <= 4 ? 4 : maxt <= 8 ? 8 : 16;  // template bucket
+  maxt = maxt <= 2 ? 2 : maxt <= 4 ? 4 : maxt <= 8 ? 8 : maxt <= 12 ? 12 : 16;  // template bucket
   int maxq = (P.n + 31) / 32;
   maxq = maxq <= 1 ? 1 : maxq <= 2 ? 2 : 4;
   const int J = P.mode == SOLVER_RBPG ? P.num_blocks : 1;
