@@ -10,40 +10,88 @@
 namespace tb {
 
 // ------------------------------------------------------------------ default lambda
-// One warp per pixel (grid-stride over pixels), lanes own columns; b broadcast from shared.
-__global__ void __launch_bounds__(256) default_lambda_kernel(const float2* __restrict__ A, int n, int m,
-                                                             const float2* __restrict__ B, long long P,
-                                                             double beta, float* __restrict__ lam) {
-  extern __shared__ float2 sb[];  // [warps][n]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  float2* bw = sb + (size_t)warp * n;
-  for (long long p = (long long)blockIdx.x * nw + warp; p < P; p += (long long)gridDim.x * nw) {
-    for (int i = lane; i < n; i += 32) bw[i] = B[(size_t)p * n + i];
-    __syncwarp();
-    float best = 0.f;
-    for (int c = lane; c < m; c += 32) {
-      float2 acc = make_float2(0.f, 0.f);
-      for (int i = 0; i < n; ++i) cfma_conj(acc, __ldg(&A[(size_t)i * m + c]), bw[i]);
-      best = fmaxf(best, cabsf(acc));
+// lambda_p = beta * max_k |(A^H b_p)_k| as a tiled complex GEMM with a max epilogue: a CTA owns 64
+// dictionary columns x 64 pixels; 16-row K slices of A and of the pixel chunk are staged in shared
+// memory and every thread accumulates a 4 x 4 (column x pixel) micro-tile (columns tc + 16 i, pixels
+// tp + 16 j: conflict-free / broadcast shared reads), so each A element fetched from HBM/L2 serves
+// 64 pixels instead of one.  The per-column sums run over the rows in order with the same fp32
+// fmaf sequence as a per-column loop; the column max is order-free, so it is merged across CTAs
+// with an integer atomicMax on the (non-negative) float bits and the result is deterministic.
+constexpr int LT_C = 64, LT_P = 64, LT_K = 16;
+
+__global__ void __launch_bounds__(256) lambda_tile_kernel(const float2* __restrict__ A, int n, int m,
+                                                          const float2* __restrict__ B, long long P,
+                                                          unsigned* __restrict__ bits) {
+  __shared__ float2 sa[LT_K][LT_C];
+  __shared__ float2 sb[LT_K][LT_P + 1];  // +1: conflict-light transposed staging stores
+  const int tid = threadIdx.x, tc = tid & 15, tp = tid >> 4;
+  const long long c0 = (long long)blockIdx.x * LT_C;
+  for (long long p0 = (long long)blockIdx.y * LT_P; p0 < P; p0 += (long long)gridDim.y * LT_P) {
+    float2 acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    for (int k0 = 0; k0 < n; k0 += LT_K) {
+      for (int e = tid; e < LT_K * LT_C; e += 256) {
+        const int kk = e / LT_C, cc = e % LT_C;
+        const long long c = c0 + cc;
+        const int i = k0 + kk;
+        sa[kk][cc] = (i < n && c < m) ? __ldg(&A[(size_t)i * m + c]) : make_float2(0.f, 0.f);
+      }
+      for (int e = tid; e < LT_K * LT_P; e += 256) {
+        const int pp = e / LT_K, kk = e % LT_K;
+        const long long p = p0 + pp;
+        const int i = k0 + kk;
+        sb[kk][pp] = (i < n && p < P) ? __ldg(&B[(size_t)p * n + i]) : make_float2(0.f, 0.f);
+      }
+      __syncthreads();
+      const int kn = min(LT_K, n - k0);
+      for (int kk = 0; kk < kn; ++kk) {
+        float2 a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sa[kk][tc + 16 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = sb[kk][tp + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cfma_conj(acc[i][j], a[i], b[j]);
+      }
+      __syncthreads();
     }
-    best = warp_maxf(best);
-    if (lane == 0) lam[p] = (float)(beta * (double)best);
-    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float best = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (c0 + tc + 16 * i < m) best = fmaxf(best, cabsf(acc[i][j]));
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(TB_FULL_MASK, best, o));
+      const long long p = p0 + tp + 16 * j;
+      if (tc == 0 && p < P) atomicMax(&bits[p], __float_as_uint(best));
+    }
   }
+}
+
+__global__ void lambda_finish_kernel(float* lam, long long P, double beta) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < P) lam[p] = (float)(beta * (double)lam[p]);
 }
 
 cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B, long long P, double beta,
                                   float* lam, int num_sms, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
-  const int warps = 8;
-  long long blocks = (P + warps - 1) / warps;
-  if (blocks > (long long)num_sms * 8) blocks = (long long)num_sms * 8;
-  size_t smem = (size_t)warps * n * sizeof(float2);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(default_lambda_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  default_lambda_kernel<<<(int)blocks, warps * 32, smem, st>>>(A, n, m, B, P, beta, lam);
+  cudaError_t e = cudaMemsetAsync(lam, 0, sizeof(float) * (size_t)P, st);  // +0.0f bits: the max identity
+  if (e != cudaSuccess) return e;
+  const long long ctiles = (m + LT_C - 1) / LT_C, pchunks = (P + LT_P - 1) / LT_P;
+  long long gy = (long long)num_sms * 8 / ctiles;
+  if (gy < 1) gy = 1;
+  if (gy > pchunks) gy = pchunks;
+  if (gy > 65535) gy = 65535;
+  if (ctiles > 0x7fffffffll) return cudaErrorInvalidValue;
+  lambda_tile_kernel<<<dim3((unsigned)ctiles, (unsigned)gy), 256, 0, st>>>(A, n, m, B, P, reinterpret_cast<unsigned*>(lam));
+  lambda_finish_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(lam, P, beta);
   return cudaGetLastError();
 }
 
@@ -192,40 +240,64 @@ cudaError_t launch_power_small(const float2* A, int n, int m, const long long* s
 
 // Multi-CTA variant for wide ranges (cfg4/cfg5 full dictionaries): host-driven iteration with
 // fixed-order partial reductions (deterministic), one convergence read-back per iteration.
+constexpr int PW_COLS = 1024;  // columns per CTA of the forward partial
 __global__ void __launch_bounds__(256) pw_forward_partial(const float2* __restrict__ A, int n, int m, long long start,
                                                           long long width, const double2* __restrict__ v,
-                                                          double inv_scale, int cols_per_cta, double2* partial) {
-  // partial[cta][i] = sum_{c in cta tile} A[i][start+c] * v[c] * inv_scale
-  const long long c0 = (long long)blockIdx.x * cols_per_cta;
-  const long long c1 = min(c0 + (long long)cols_per_cta, width);
+                                                          double inv_scale, double2* partial) {
+  // partial[cta][i] = sum_{c in cta tile} A[i][start+c] * v[c] * inv_scale.  The v tile is staged
+  // once in shared memory; each warp walks its rows with four independent accumulator chains so
+  // four coalesced A loads are in flight per lane (the kernel is an HBM stream of A).
+  __shared__ double2 sv[PW_COLS];
+  const long long c0 = (long long)blockIdx.x * PW_COLS;
+  const int len = (int)min((long long)PW_COLS, width - c0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = threadIdx.x; c < PW_COLS; c += blockDim.x) sv[c] = c < len ? v[c0 + c] : make_double2(0.0, 0.0);
+  __syncthreads();
   for (int i = warp; i < n; i += nw) {
-    double re = 0.0, im = 0.0;
-    for (long long c = c0 + lane; c < c1; c += 32) {
-      float2 a = A[(size_t)i * m + start + c];
-      double2 x = v[c];
-      re += (double)a.x * x.x - (double)a.y * x.y;
-      im += (double)a.x * x.y + (double)a.y * x.x;
+    const float2* arow = A + (size_t)i * m + start + c0;
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    int c = lane;
+    for (; c + 96 < len; c += 128) {
+      float2 a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = __ldg(arow + c + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 x = sv[c + 32 * u];
+        re[u] = fma((double)a[u].x, x.x, fma(-(double)a[u].y, x.y, re[u]));
+        im[u] = fma((double)a[u].x, x.y, fma((double)a[u].y, x.x, im[u]));
+      }
     }
-    re = warp_sum(re);
-    im = warp_sum(im);
-    if (lane == 0) partial[(size_t)blockIdx.x * n + i] = make_double2(re * inv_scale, im * inv_scale);
+    for (; c < len; c += 32) {
+      const float2 a = __ldg(arow + c);
+      const double2 x = sv[c];
+      re[0] = fma((double)a.x, x.x, fma(-(double)a.y, x.y, re[0]));
+      im[0] = fma((double)a.x, x.y, fma((double)a.y, x.x, im[0]));
+    }
+    double r = warp_sum((re[0] + re[1]) + (re[2] + re[3]));
+    double q = warp_sum((im[0] + im[1]) + (im[2] + im[3]));
+    if (lane == 0) partial[(size_t)blockIdx.x * n + i] = make_double2(r * inv_scale, q * inv_scale);
   }
 }
 
-__global__ void pw_reduce_w(const double2* partial, int nparts, int n, double2* w, double* cur) {
+__global__ void __launch_bounds__(256) pw_reduce_w(const double2* partial, int nparts, int n, double2* w, double* cur) {
+  // w[i] = sum over the CTA partials (one warp per row, lanes stride the partials: fixed order)
   __shared__ double red[32];
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < n; i += nw) {
     double re = 0.0, im = 0.0;
-    for (int p = 0; p < nparts; ++p) {
-      double2 t = partial[(size_t)p * n + i];
+    for (int p = lane; p < nparts; p += 32) {
+      const double2 t = partial[(size_t)p * n + i];
       re += t.x;
       im += t.y;
     }
-    w[i] = make_double2(re, im);
-    s += re * re + im * im;
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == 0) w[i] = make_double2(re, im);
   }
+  __syncthreads();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += w[i].x * w[i].x + w[i].y * w[i].y;
   s = block_sum(s, red);
   if (threadIdx.x == 0) *cur = s;
 }
@@ -236,15 +308,30 @@ __global__ void __launch_bounds__(256) pw_adjoint(const float2* __restrict__ A, 
   __shared__ double red[32];
   double s = 0.0;
   for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < width; c += (long long)gridDim.x * blockDim.x) {
-    double re = 0.0, im = 0.0;
-    for (int i = 0; i < n; ++i) {
-      float2 a = A[(size_t)i * m + start + c];
-      double2 ww = w[i];
-      re += (double)a.x * ww.x + (double)a.y * ww.y;
-      im += (double)a.x * ww.y - (double)a.y * ww.x;
+    // four independent row chains: four coalesced A loads in flight per thread
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    const float2* acol = A + start + c;
+    int i = 0;
+    for (; i + 4 <= n; i += 4) {
+      float2 a[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[q] = __ldg(acol + (size_t)(i + q) * m);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 ww = w[i + q];
+        re[q] = fma((double)a[q].x, ww.x, fma((double)a[q].y, ww.y, re[q]));
+        im[q] = fma((double)a[q].x, ww.y, fma(-(double)a[q].y, ww.x, im[q]));
+      }
     }
-    u[c] = make_double2(re, im);
-    s += re * re + im * im;
+    for (; i < n; ++i) {
+      const float2 a = __ldg(acol + (size_t)i * m);
+      const double2 ww = w[i];
+      re[0] = fma((double)a.x, ww.x, fma((double)a.y, ww.y, re[0]));
+      im[0] = fma((double)a.x, ww.y, fma(-(double)a.y, ww.x, im[0]));
+    }
+    const double rr = (re[0] + re[1]) + (re[2] + re[3]), ii = (im[0] + im[1]) + (im[2] + im[3]);
+    u[c] = make_double2(rr, ii);
+    s += rr * rr + ii * ii;
   }
   s = block_sum(s, red);
   if (threadIdx.x == 0) nrm_partial[blockIdx.x] = s;
@@ -266,8 +353,7 @@ cudaError_t power_iter_large(const float2* A, int n, int m, long long start, lon
     // handled by the small kernel path in the caller
     return cudaErrorInvalidValue;
   }
-  const int cols_per_cta = 4096;
-  const int nparts = (int)((width + cols_per_cta - 1) / cols_per_cta);
+  const int nparts = (int)((width + PW_COLS - 1) / PW_COLS);
   const int adj_blocks = num_sms * 4;
   double2 *partial = nullptr, *w = nullptr;
   double *scal = nullptr, *nrm_part = nullptr;
@@ -280,7 +366,7 @@ cudaError_t power_iter_large(const float2* A, int n, int m, long long start, lon
   double inv = 1.0;  // v holds the unnormalised u after the first iteration; scale folded in
   bool first = true;
   for (int it = 0; it < max_iter; ++it) {
-    pw_forward_partial<<<nparts, 256, 0, st>>>(A, n, m, start, width, first ? v : u, inv, cols_per_cta, partial);
+    pw_forward_partial<<<nparts, 256, 0, st>>>(A, n, m, start, width, first ? v : u, inv, partial);
     pw_reduce_w<<<1, 256, 0, st>>>(partial, nparts, n, w, scal);
     pw_adjoint<<<adj_blocks, 256, 0, st>>>(A, n, m, start, width, w, u, nrm_part);
     pw_reduce_norm<<<1, 256, 0, st>>>(nrm_part, adj_blocks, scal + 1);
