@@ -189,7 +189,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       for (int j = lane; j < J; j += 32) l1blk[j] = 0.0;
     if (lane == 0) ring[0] = F;
     int ridx = 0;  // k mod (STOP_WINDOW + 1), kept incrementally
-    if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride] = F;
+    double* const hrow = P.hist ? P.hist + (size_t)p * P.hist_stride : nullptr;  // all lanes store F (same value)
+    if (hrow) hrow[0] = F;
     const uint64_t seed = RB ? P.seeds[p] : 0ull;
     uint64_t* rbuf = reinterpret_cast<uint64_t*>(l1blk + J);  // 32 buffered Philox outputs
     int* clist = reinterpret_cast<int*>(rbuf + 32);               // nonzero columns of zs, ascending
@@ -238,31 +239,36 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       unsigned masks[MAXT];
       bool any_dy = false;
       int cnt = 0;  // RBPG: compacted nonzero count in zs / clist
+      // Column passes are branch-free: lanes past the range read a valid column (cs) and their
+      // results are masked, so no divergent-branch reconvergence is paid per pass; passes that lie
+      // entirely past the range are skipped with a warp-uniform test.
 #pragma unroll
       for (int t = 0; t < MAXT; ++t) {
+        masks[t] = 0u;
+        if (t > 0 && 32 * t >= width) continue;
         const int cl = lane + 32 * t;
+        const bool act = cl < width;
+        const int col = cs + (act ? cl : 0);
+        const double2 xv = xs[col];
+        double2 yv = xv;
+        if (!ista) {
+          // y = x + m_k (x - prev) with the extrapolation memory kept as d = x - prev in fp32;
+          // d is exactly 0 after a rejected visit, so `np.any(dy)` (solver.py:291) is preserved
+          const float2 dv = ds[col];
+          yv.x = fma(mk, (double)dv.x, xv.x);
+          yv.y = fma(mk, (double)dv.y, xv.y);
+        }
         bool nz = false;
         double2 dyv = make_double2(0.0, 0.0);
-        if (cl < width) {
-          const double2 xv = xs[cs + cl];
-          double2 yv = xv;
-          if (!ista) {
-            // y = x + m_k (x - prev) with the extrapolation memory kept as d = x - prev in fp32;
-            // d is exactly 0 after a rejected visit, so `np.any(dy)` (solver.py:291) is preserved
-            const float2 dv = ds[cs + cl];
-            yv.x = fma(mk, (double)dv.x, xv.x);
-            yv.y = fma(mk, (double)dv.y, xv.y);
-          }
-          if (RB) {
-            dyv = make_double2(yv.x - xv.x, yv.y - xv.y);
-            nz = (dyv.x != 0.0) || (dyv.y != 0.0);
-          }
+        if (RB) {
+          dyv = make_double2(yv.x - xv.x, yv.y - xv.y);
+          nz = act && ((dyv.x != 0.0) || (dyv.y != 0.0));
         }
         masks[t] = __ballot_sync(TB_FULL_MASK, nz);
         if (RB && nz) {
           const int pos = cnt + __popc(masks[t] & lt_mask);
           zs[pos] = dyv;
-          clist[pos] = cs + cl;
+          clist[pos] = col;
         }
         cnt += __popc(masks[t]);
         any_dy |= masks[t] != 0u;
@@ -330,46 +336,46 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         cnt = 0;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
+          masks[t] = 0u;
+          if (t > 0 && 32 * t >= width) continue;
           const int cl = lane + 32 * t;
-          bool nz = false;
-          double2 dw = make_double2(0.0, 0.0);
-          if (cl < width) {
-            // y = x + m_k d recomputed from shared memory (keeps registers for occupancy)
-            const double2 xv = xs[cs + cl];
-            double2 yv = xv;
-            if (!ista) {
-              const float2 dv = ds[cs + cl];
-              yv.x = fma(mk, (double)dv.x, xv.x);
-              yv.y = fma(mk, (double)dv.y, xv.y);
-            }
-            const double2 v = make_double2(fma(-alpha, (double)g[t].x, yv.x), fma(-alpha, (double)g[t].y, yv.y));
-            const double mag2 = fma(v.x, v.x, v.y * v.y);
-            double2 zz = make_double2(0.0, 0.0);
-            if (mag2 > tau2) {  // soft_threshold: zero iff |v| <= tau (prox.py:82-96)
-              // scale 1 - tau/|v| and |z| = |v| - tau from one fp64 reciprocal square root
-#if TB_WS_RSQRT
-              const double rs = rsqrt(mag2);
-              const double sc = fma(-tau, rs, 1.0);
-              zz = make_double2(v.x * sc, v.y * sc);
-              red[1] += fma(mag2, rs, -tau);
-#else
-              const double mag = sqrt(mag2);
-              const double sc = 1.0 - tau / mag;
-              zz = make_double2(v.x * sc, v.y * sc);
-              red[1] += mag * sc;
-#endif
-            }
-            if (RB) z[t] = zz;
-            const double2 d = make_double2(zz.x - yv.x, zz.y - yv.y);
-            red[0] += fma(d.x, d.x, d.y * d.y);
-            dw = RB ? d : zz;
-            nz = (dw.x != 0.0) || (dw.y != 0.0);
+          const bool act = cl < width;
+          const int col = cs + (act ? cl : 0);
+          // y = x + m_k d recomputed from shared memory (keeps registers for occupancy)
+          const double2 xv = xs[col];
+          double2 yv = xv;
+          if (!ista) {
+            const float2 dv = ds[col];
+            yv.x = fma(mk, (double)dv.x, xv.x);
+            yv.y = fma(mk, (double)dv.y, xv.y);
           }
+          const double2 v = make_double2(fma(-alpha, (double)g[t].x, yv.x), fma(-alpha, (double)g[t].y, yv.y));
+          const double mag2 = fma(v.x, v.x, v.y * v.y);
+          double2 zz = make_double2(0.0, 0.0);
+          if (act && mag2 > tau2) {  // soft_threshold: zero iff |v| <= tau (prox.py:82-96)
+            // scale 1 - tau/|v| and |z| = |v| - tau from one fp64 reciprocal square root
+#if TB_WS_RSQRT
+            const double rs = rsqrt(mag2);
+            const double sc = fma(-tau, rs, 1.0);
+            zz = make_double2(v.x * sc, v.y * sc);
+            red[1] += fma(mag2, rs, -tau);
+#else
+            const double mag = sqrt(mag2);
+            const double sc = 1.0 - tau / mag;
+            zz = make_double2(v.x * sc, v.y * sc);
+            red[1] += mag * sc;
+#endif
+          }
+          if (RB) z[t] = zz;
+          const double2 d = make_double2(zz.x - yv.x, zz.y - yv.y);
+          red[0] += act ? fma(d.x, d.x, d.y * d.y) : 0.0;
+          const double2 dw = RB ? d : zz;
+          const bool nz = act && ((dw.x != 0.0) || (dw.y != 0.0));
           masks[t] = __ballot_sync(TB_FULL_MASK, nz);
           if (nz) {
             const int pos = cnt + __popc(masks[t] & lt_mask);
             zs[pos] = dw;
-            clist[pos] = cs + cl;
+            clist[pos] = col;
           }
           cnt += __popc(masks[t]);
         }
@@ -421,8 +427,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       if (!ok) {
         // RBPG appends F before breaking (solver.py:311-314); ISTA/FISTA do not (solver.py:357-361)
         if (RB) {
-          if (lane == 0) ring[ridx] = F;
-          if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride + k] = F;
+          ring[ridx] = F;
+          if (hrow) hrow[k] = F;
         }
         status = STATUS_LINE_SEARCH_FAILURE;
         stopped = true;
@@ -440,15 +446,13 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         const bool accept = cand <= F;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
+          if (t > 0 && 32 * t >= width) continue;
           const int cl = lane + 32 * t;
           if (cl < width) {
-            if (accept) {
-              const double2 xv = xs[cs + cl], zv = z[RB ? t : 0];
-              ds[cs + cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
-              xs[cs + cl] = zv;
-            } else {
-              ds[cs + cl] = make_float2(0.f, 0.f);  // prev_b <- x_b (solver.py:325)
-            }
+            // accept: prev_b <- x_b, x_b <- z_b; reject: prev_b <- x_b (solver.py:318-325)
+            const double2 xv = xs[cs + cl], zv = accept ? z[RB ? t : 0] : xv;
+            ds[cs + cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
+            xs[cs + cl] = zv;
           }
         }
         if (accept) {
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           }
           l1 = l1_new;
           F = cand;
-          if (lane == 0) l1blk[blk] = l1z;
+          l1blk[blk] = l1z;
         }
       } else {
         // x_prev <- x, x <- z, F = ||A z - b||^2 + lambda ||z||_1 (solver.py:362-364)
@@ -467,6 +471,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         int base = 0;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
+          if (t > 0 && 32 * t >= width) break;
           const int cl = lane + 32 * t;
           if (cl < width) {
             const double2 xv = xs[cl];
@@ -487,8 +492,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         F = fzs + lamd * l1z;
       }
       // ---- history, failure and window stop (solver.py:326-336, 366-374)
-      if (lane == 0) ring[ridx] = F;
-      if (P.hist && lane == 0) P.hist[(size_t)p * P.hist_stride + k] = F;
+      ring[ridx] = F;  // every lane stores the same value (no divergent branch)
+      if (hrow) hrow[k] = F;
       __syncwarp();
       if (!isfinite(F)) {
         status = STATUS_NUMERICAL_FAILURE;
