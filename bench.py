@@ -317,7 +317,7 @@ def run_b200(args):
                 what = f"{sample} pixels of cfg{args.config}, {args.backend}, {fixed} fixed iterations each (+ per-solve power iterations), rate scaled by {fixed}/{float(its.mean()):.0f} (GPU mean iterations)"
             else:
                 # whole solves (max_iters=500, tol=1e-6) of the first pixels, cycling over the batch.
-                # A short calibration pass sizes the timed sample to ~12 s of wall time on all cores.
+                # The sample grows until one timed pass takes ~12 s of wall time on all cores.
                 kw = dict(max_iters=500, tol=1e-6, num_blocks=8)
 
                 def timed(count):
@@ -326,9 +326,13 @@ def run_b200(args):
                     seeds_h = np.array([O.derive_seed(2018, int(p)) for p in idx], dtype=np.uint64)
                     return cpu_baseline(_Rows(batch, idx), args.backend, count, lam_h, seeds_h, cores, kw)
 
-                rate, _, _ = timed(cores * 4)
-                sample = args.cpu_sample or int(min(max(rate * 12.0, cores * 8), 200_000))
-                v, wall, _ = timed(sample)
+                # grow the sample until one pass takes >= 8 s (pool start-up is a few 0.1 s)
+                sample = args.cpu_sample or cores * 16
+                while True:
+                    v, wall, _ = timed(sample)
+                    if args.cpu_sample or wall >= 8.0 or sample >= 200_000:
+                        break
+                    sample = int(min(sample * 12.0 / max(wall, 0.25), 200_000))
                 what = f"{sample} pixels of cfg{args.config} (ids 0.. cycling over the batch), {args.backend}, whole solves"
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": f"{what}, process pool x{cores}, {wall:.1f} s wall, per-solve power iterations as solver.py:267/344"}
     if world > 1:

@@ -103,6 +103,17 @@ class _GridDev:
         self.motion = torch.from_numpy(mot).to(device)
 
 
+def _grid_dev(d: Dictionary, grid: ParameterGrid) -> _GridDev:
+    """Device copy of the grid axes, cached on the dictionary: a pageable host->device copy per
+    call would block the host behind the solver kernel already queued on the stream."""
+    cache = d.__dict__.setdefault("_grid_cache", {})
+    key = (np.asarray(grid.elevation, dtype=np.float64).tobytes(), tuple(np.asarray(a, dtype=np.float64).tobytes() for a in grid.motion_axes))
+    g = cache.get(key)
+    if g is None:
+        g = cache[key] = _GridDev(grid, d.device)
+    return g
+
+
 def select_batch(d: Dictionary, x_hat, pixels, grid: ParameterGrid, k_max: int, params_per_scatterer: int | None = None) -> BatchEstimates:
     """detect_support -> model_select -> estimate_params for every pixel (slimmer.py:77-190)."""
     torch = _torch()
@@ -113,7 +124,7 @@ def select_batch(d: Dictionary, x_hat, pixels, grid: ParameterGrid, k_max: int, 
     b = d._pixels(pixels)
     p = int(b.shape[0])
     ppsc = 3 + len(grid.motion_axes) if params_per_scatterer is None else int(params_per_scatterer)
-    g = _GridDev(grid, d.device)
+    g = _grid_dev(d, grid)
     dev = d.device
     order = torch.empty(p, dtype=torch.int32, device=dev)
     support = torch.empty((p, k_max), dtype=torch.int64, device=dev)
