@@ -209,6 +209,7 @@ def run_b200(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ks, ke = [], []
+    launches0 = tb._lib.launch_count()
     iters_total = 0
     ev0.record(stream)
     for _ in range(args.steps):
@@ -224,6 +225,7 @@ def run_b200(args):
         ke.append(b)
         iters_total += sol.iterations  # device tensor accumulate (no sync)
     ev1.record(stream)
+    launches = tb._lib.launch_count() - launches0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -294,7 +296,7 @@ def run_b200(args):
                 "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms_per_step,
             },
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
-            "gpu_launches": args.steps * (4 if args.backend == "rbpg" else 3),
+            "gpu_launches": launches,
             "clocks": clk,
             "solver_stats": {"mean_iterations": float(its.mean()), "converged_frac": float((st == 0).mean()), "max_iters_frac": float((st == 1).mean())},
         }
@@ -390,8 +392,10 @@ def run_cfg5_sharded(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
+    launches0 = tb._lib.launch_count()
     for _ in range(args.steps):
         sol = step()
+    launches = tb._lib.launch_count() - launches0
     e1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -402,6 +406,30 @@ def run_cfg5_sharded(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # end to end: the RHS stack from pinned host memory in, objective/iterations/status back out
+    pix_host = torch.from_numpy(batch.pixels).pin_memory()
+    e2e_ms = []
+    d2h = 0
+    for _ in range(2):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        pix_dev = pix_host.to(dev, non_blocking=True)
+        s2 = solve_column_sharded([shard], pix_dev, lam, scfg, seeds=seeds, reduce_fn=reduce_fn)[0]
+        outs = [s2.objective_final, s2.iterations, s2.status]
+        host = [o.to("cpu", non_blocking=True) for o in outs]
+        a1.record()
+        torch.cuda.synchronize()
+        d2h = sum(o.numel() * o.element_size() for o in outs)
+        e2e_ms.append(a0.elapsed_time(a1))
+    e2e_step = float(np.median(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
     its = sol.iterations.cpu().numpy()
     pix_iters = float(its.sum())
     flop_pi = flops_per_pixel_iteration(args.backend, n, m, 8)
@@ -416,7 +444,8 @@ def run_cfg5_sharded(args):
                        "step": "tiled solve of all RHS (rounds driven from Python, NCCL all-reduce between pass and update)"},
             "roofline": {"bound": "fp32", "kernel": "tiled_pass_kernel (+ prep/reduce/update)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src, "note": "achieved over the whole step, all ranks' work / max-rank time / world"},
-            "gpu_launches": None, "clocks": clk,
+            "e2e": {"value": P / (e2e_step / 1000.0), "unit": UNIT, "h2d_bytes_per_step": pix_host.numel() * pix_host.element_size(), "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
+            "gpu_launches": launches, "clocks": clk,
             "solver_stats": {"mean_iterations": float(its.mean()), "converged_frac": float((sol.status.cpu().numpy() == 0).mean())},
         }
         line["roofline"]["achieved"] = achieved / world

@@ -58,6 +58,9 @@ typedef struct tb_solver_config {
 
 const char* tb_version(void);
 const char* tb_last_error(void);
+/* Number of kernels this library has launched since it was loaded (all entry points, all
+   devices).  Instrumentation for the benchmark's gpu_launches claim; no reference counterpart. */
+int64_t tb_launch_count(void);
 
 /* Objective.dictionary (prox.py:25-63): copy a device complex64 [n, m] row-major matrix
  * (row = acquisition, column = flat grid index, model.py:317-323) into a new context. */

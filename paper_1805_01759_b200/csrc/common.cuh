@@ -8,6 +8,9 @@
 
 namespace tb {
 
+// Host-side count of this library's kernel launches (tb_launch_count, include/tomobpdn_b200.h).
+void count_launch();
+
 // ---------------------------------------------------------------- complex64 arithmetic
 struct __align__(8) c64 {
   float x, y;

@@ -326,6 +326,7 @@ static cudaError_t launch_g(const SolveParams& P, int warps, size_t smem, int gr
   auto k = rbpg_group_kernel<G, MAXT, MAXQ, ASMEM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  count_launch();
   k<<<grid, warps * 32, smem, st>>>(P);
   return cudaGetLastError();
 }

@@ -271,6 +271,7 @@ cudaError_t launch_select(const SelectParams& S, int num_sms, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   long long blocks = (S.num_pixels + warps - 1) / warps;
   if (blocks > (long long)num_sms * 16) blocks = (long long)num_sms * 16;
+  count_launch();
   select_kernel<<<(int)blocks, warps * 32, smem, st>>>(S);
   return cudaGetLastError();
 }

@@ -90,7 +90,9 @@ cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B
   if (gy > pchunks) gy = pchunks;
   if (gy > 65535) gy = 65535;
   if (ctiles > 0x7fffffffll) return cudaErrorInvalidValue;
+  count_launch();
   lambda_tile_kernel<<<dim3((unsigned)ctiles, (unsigned)gy), 256, 0, st>>>(A, n, m, B, P, reinterpret_cast<unsigned*>(lam));
+  count_launch();
   lambda_finish_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(lam, P, beta);
   return cudaGetLastError();
 }
@@ -115,6 +117,7 @@ __global__ void derive_seeds_kernel(uint64_t run_seed, long long first, long lon
 
 cudaError_t launch_derive_seeds(uint64_t run_seed, long long first, long long P, uint64_t* seeds, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
+  count_launch();
   derive_seeds_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(run_seed, first, P, seeds);
   return cudaGetLastError();
 }
@@ -232,6 +235,7 @@ cudaError_t launch_power_small(const float2* A, int n, int m, const long long* s
   if (e != cudaSuccess) return e;
   size_t smem = (size_t)n * sizeof(double2);
   if (smem > 48 * 1024) cudaFuncSetAttribute(power_iter_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  count_launch();
   power_iter_small_kernel<<<num_ranges, 256, smem, st>>>(A, n, m, dr, v, uscratch, max_iter, rtol, out_dev);
   e = cudaGetLastError();
   cudaFreeAsync(dr, st);
@@ -366,9 +370,13 @@ cudaError_t power_iter_large(const float2* A, int n, int m, long long start, lon
   double inv = 1.0;  // v holds the unnormalised u after the first iteration; scale folded in
   bool first = true;
   for (int it = 0; it < max_iter; ++it) {
+    count_launch();
     pw_forward_partial<<<nparts, 256, 0, st>>>(A, n, m, start, width, first ? v : u, inv, partial);
+    count_launch();
     pw_reduce_w<<<1, 256, 0, st>>>(partial, nparts, n, w, scal);
+    count_launch();
     pw_adjoint<<<adj_blocks, 256, 0, st>>>(A, n, m, start, width, w, u, nrm_part);
+    count_launch();
     pw_reduce_norm<<<1, 256, 0, st>>>(nrm_part, adj_blocks, scal + 1);
     e = cudaMemcpyAsync(host, scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -429,6 +437,7 @@ __global__ void steering_kernel(const double* __restrict__ xi, const double* __r
 cudaError_t launch_steering(const double* xi, const double* eta, int n, int n_axes, const double* elev, const double* motion,
                             int ms0, int ms1, long long col0, long long ncols, double sign, float2* out, int num_sms, cudaStream_t st) {
   if (n <= 0 || ncols <= 0) return cudaSuccess;
+  count_launch();
   steering_kernel<<<num_sms * 8, 256, 0, st>>>(xi, eta, n, n_axes, elev, motion, ms0, ms1, col0, ncols, sign, out);
   return cudaGetLastError();
 }
@@ -472,6 +481,7 @@ cudaError_t launch_apply_filter(const double2* W, int n, int m, const float2* B,
     cudaError_t e = cudaFuncSetAttribute(apply_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
+  count_launch();
   apply_filter_kernel<<<(int)blocks, warps * 32, smem, st>>>(W, n, m, B, P, X);
   return cudaGetLastError();
 }

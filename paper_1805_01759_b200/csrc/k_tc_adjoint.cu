@@ -165,6 +165,7 @@ extern "C" int tb_tc_adjoint_proto(const void* A, int n, int m, int col0, const 
   if (n < 4 || (2 * n) % 8 != 0 || n > 64) return 1;
   const size_t smem = (size_t)(2 * 128 + 2 * 32) * (2 * n) * 4;
   cudaFuncSetAttribute(tb::tc_adjoint_proto_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tb::count_launch();
   tb::tc_adjoint_proto_kernel<<<1, 128, smem, (cudaStream_t)stream>>>((const float2*)A, n, m, col0, (const float2*)R, (float2*)G, passes);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }

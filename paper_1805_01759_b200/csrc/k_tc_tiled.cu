@@ -277,18 +277,21 @@ int tc_chunks(int n) { return (n + TC_KC - 1) / TC_KC; }
 
 cudaError_t tc_pack_dictionary(const float2* A, int n, int m, int J, const int* bstart_dev, const int* tile_base_dev, int nck,
                                float* Apk, long long total_tiles, int num_sms, cudaStream_t st) {
+  count_launch();
   tc_pack_dictionary_kernel<<<num_sms * 8, 256, 0, st>>>(A, n, m, J, bstart_dev, tile_base_dev, nck, Apk, total_tiles);
   return cudaGetLastError();
 }
 
 cudaError_t tc_adjoint_round(const TiledParams& T, const float* Apk, float* Rpk, const int* tile_base_dev, int nck,
                              int max_tiles, int tiles_per_split, int max_splits, float2* G, cudaStream_t st) {
+  count_launch();
   tc_pack_pixels_kernel<<<max_tiles, 256, 0, st>>>(T, nck, Rpk);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = 2 * (size_t)TC_STAGE_BYTES;
   e = cudaFuncSetAttribute(tc_adjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  count_launch();
   tc_adjoint_kernel<<<dim3(max_tiles, max_splits), 128, smem, st>>>(T, Apk, Rpk, tile_base_dev, nck, tiles_per_split, G);
   return cudaGetLastError();
 }

@@ -563,14 +563,17 @@ __global__ void tiled_finish_kernel(const TiledParams T) {
 static inline int warp_grid(int P) { return (P + 7) / 8; }
 
 cudaError_t tiled_init(const TiledParams& T, cudaStream_t st) {
+  count_launch();
   tiled_init_kernel<<<warp_grid(T.P), 256, 0, st>>>(T);
   return cudaGetLastError();
 }
 
 cudaError_t tiled_prep(const TiledParams& T, cudaStream_t st) {
+  count_launch();
   tiled_prep_kernel<<<warp_grid(T.P), 256, 0, st>>>(T);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  count_launch();
   tiled_schedule_kernel<<<1, 1024, 3 * T.J * sizeof(int), st>>>(T);
   return cudaGetLastError();
 }
@@ -581,18 +584,24 @@ cudaError_t tiled_pass(const TiledParams& T, int num_sms, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(tiled_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((T.P + TL_PT - 1) / TL_PT + T.J, T.max_splits);
+  count_launch();
   tiled_pass_kernel<<<grid, TL_THREADS, smem, st>>>(T);
   return cudaGetLastError();
 }
 
 cudaError_t tiled_reduce(const TiledParams& T, cudaStream_t st) {
+  count_launch();
   tiled_reduce_kernel<<<warp_grid(T.P), 256, 0, st>>>(T);
   return cudaGetLastError();
 }
 
 cudaError_t tiled_update(const TiledParams& T, cudaStream_t st) {
   const bool rb = T.mode == SOLVER_RBPG;
-  if (rb) tiled_commit_clear_kernel<<<(T.P + 255) / 256, 256, 0, st>>>(T);
+  if (rb) {
+    count_launch();
+    tiled_commit_clear_kernel<<<(T.P + 255) / 256, 256, 0, st>>>(T);
+  }
+  count_launch();
   tiled_update_kernel<<<warp_grid(T.P), 256, 0, st>>>(T);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !rb) return e;
@@ -602,6 +611,7 @@ cudaError_t tiled_update(const TiledParams& T, cudaStream_t st) {
   int chunks = (maxw + 2047) / 2048;  // ~8 columns per thread
   chunks = chunks < 1 ? 1 : chunks > 64 ? 64 : chunks;
   dim3 grid(T.P, chunks);
+  count_launch();
   tiled_commit_kernel<<<grid, 256, 0, st>>>(T);
   return cudaGetLastError();
 }
@@ -610,6 +620,7 @@ cudaError_t tiled_finish(const TiledParams& T, cudaStream_t st) {
   int chunks = (T.m + 2047) / 2048;
   chunks = chunks < 1 ? 1 : chunks > 64 ? 64 : chunks;
   dim3 grid(T.P, chunks);
+  count_launch();
   tiled_finish_kernel<<<grid, 256, 0, st>>>(T);
   return cudaGetLastError();
 }

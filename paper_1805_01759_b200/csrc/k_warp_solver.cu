@@ -532,6 +532,7 @@ static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int gr
   auto k = warp_solver_kernel<RB, MAXT, MAXQ, ASMEM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  count_launch();
   k<<<grid, warps * 32, smem, st>>>(P);
   return cudaGetLastError();
 }

@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -101,8 +102,12 @@ static int fail(int code, const char* fmt, ...) {
     if (_e != cudaSuccess) return fail(TB_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
   } while (0)
 
+static std::atomic<long long> g_launches{0};
+void tb::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 extern "C" {
 
+int64_t tb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 const char* tb_version(void) { return "tomobpdn_b200 0.1.0 sm_100a"; }
 const char* tb_last_error(void) { return g_err.c_str(); }
 
