@@ -245,22 +245,33 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
         cfma_conj(acc[1][j], a, rbv);
       }
     }
-    // ---- epilogue: extrapolation + soft threshold in fp64 against the HBM state
+    // ---- epilogue: extrapolation + soft threshold in fp64 against the HBM state; all-zero state
+    //      tiles (occupancy 0) are not read, all-zero candidate tiles are not written
+    const int ft = T.ftile[b] + (col0 - c_begin) / TL_CT;
+    const size_t PN = (size_t)T.P * T.NT;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int slot = 2 * pg + q;
       const int p = sPid[slot];
       unsigned long long nzm = 0ull;  // this half-warp's pixel: nonzero columns of the tile
+      bool ox = false, op = false;
+      if (p >= 0) {
+        ox = T.occ[sRx[slot] * PN + (size_t)p * T.NT + ft] != 0;
+        op = !ista && T.occ[sRp[slot] * PN + (size_t)p * T.NT + ft] != 0;
+      }
+      double2 zr[4];
+      bool zany = false;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int c = cg + 16 * j;
         double2 w = make_double2(0.0, 0.0);
+        zr[j] = make_double2(0.0, 0.0);
         if (p >= 0 && c < ncols) {
           const int gc = col0 + c;
-          const double2 xv = xrow(T, sRx[slot], p)[gc];
+          const double2 xv = ox ? xrow(T, sRx[slot], p)[gc] : make_double2(0.0, 0.0);
           double2 y = xv;
           if (!ista) {
-            const double2 pv = xrow(T, sRp[slot], p)[gc];
+            const double2 pv = op ? xrow(T, sRp[slot], p)[gc] : make_double2(0.0, 0.0);
             const double mk = sMk[slot];
             y = make_double2(fma(mk, xv.x - pv.x, xv.x), fma(mk, xv.y - pv.y, xv.y));
           }
@@ -274,7 +285,8 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
             z = make_double2(v.x * sc, v.y * sc);
             sz1[q] += mag * sc;
           }
-          xrow(T, sRz[slot], p)[gc] = z;
+          zr[j] = z;
+          zany |= (z.x != 0.0) || (z.y != 0.0);
           const double2 d = make_double2(z.x - y.x, z.y - y.y);
           sd2[q] += fma(d.x, d.x, d.y * d.y);
           sy2[q] += fma(y.x, y.x, y.y * y.y);
@@ -286,6 +298,17 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
         nzm |= (unsigned long long)((lane < 16 ? bits : bits >> 16) & 0xFFFFu) << (16 * j);
       }
       if (cg == 0) sMask[slot] = nzm;
+      const unsigned zb = __ballot_sync(TB_FULL_MASK, zany);
+      const bool tile_nz = ((lane < 16 ? zb : zb >> 16) & 0xFFFFu) != 0u;
+      if (p >= 0) {
+        if (tile_nz) {
+          double2* zrow = xrow(T, sRz[slot], p) + col0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (cg + 16 * j < ncols) zrow[cg + 16 * j] = zr[j];
+        }
+        if (cg == 0) T.occ[sRz[slot] * PN + (size_t)p * T.NT + ft] = tile_nz ? 1 : 0;
+      }
     }
     __syncthreads();
     // ---- forward partial, fp64 (lane = row, 16 pixels per thread).  Dense over the union of the
@@ -526,18 +549,38 @@ __global__ void tiled_update_kernel(const TiledParams T) {
 // prev_b <- x_b for every pixel that finished a visit this round, x_b <- z_b if it was accepted
 // (solver.py:318-325); grid over (pixel, column chunk) so wide blocks copy at HBM bandwidth.
 __global__ void tiled_commit_kernel(const TiledParams T) {
+  // one warp per occupancy tile of the drawn block; only nonzero tiles move data, the occupancy
+  // bits move with them (prev_b <- x_b, then x_b <- z_b on accept)
   const int p = blockIdx.x;
   const int flag = T.commit[p];
   if (flag == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int b = T.blk[p];
   const int c0 = T.bstart[b], c1 = T.bstart[b + 1];
-  double2* xr = xrow(T, T.roles[3 * p + 0], p);
-  double2* pr = xrow(T, T.roles[3 * p + 1], p);
-  const double2* zr = xrow(T, T.roles[3 * p + 2], p);
-  for (int c = c0 + blockIdx.y * blockDim.x + threadIdx.x; c < c1; c += gridDim.y * blockDim.x) {
-    const double2 xv = xr[c];
-    pr[c] = xv;
-    if (flag == 2) xr[c] = zr[c];
+  const int rx = T.roles[3 * p + 0], rp = T.roles[3 * p + 1], rz = T.roles[3 * p + 2];
+  double2* xr = xrow(T, rx, p);
+  double2* pr = xrow(T, rp, p);
+  const double2* zr = xrow(T, rz, p);
+  const size_t PN = (size_t)T.P * T.NT;
+  unsigned char* ox = T.occ + rx * PN + (size_t)p * T.NT + T.ftile[b];
+  unsigned char* op = T.occ + rp * PN + (size_t)p * T.NT + T.ftile[b];
+  const unsigned char* oz = T.occ + rz * PN + (size_t)p * T.NT + T.ftile[b];
+  const int ntile = (c1 - c0 + TL_CT - 1) / TL_CT;
+  for (int t = blockIdx.y * nw + warp; t < ntile; t += gridDim.y * nw) {
+    const unsigned char fx = ox[t], fz = oz[t];
+#pragma unroll
+    for (int h = 0; h < TL_CT / 32; ++h) {
+      const int c = c0 + t * TL_CT + lane + 32 * h;
+      if (c < c1) {
+        if (fx) pr[c] = xr[c];
+        if (flag == 2 && fz) xr[c] = zr[c];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      op[t] = fx;
+      if (flag == 2) ox[t] = fz;
+    }
   }
 }
 
@@ -548,11 +591,25 @@ __global__ void tiled_commit_clear_kernel(const TiledParams T) {
 
 // ------------------------------------------------------------------ finish
 __global__ void tiled_finish_kernel(const TiledParams T) {
+  // complex64 x_hat from the fp64 iterate, one warp per occupancy tile (zero tiles not read)
   const int p = blockIdx.x;
-  const double2* xr = xrow(T, T.roles[3 * p + 0], p);
-  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < T.m; c += gridDim.y * blockDim.x) {
-    const double2 v = xr[c];
-    T.X[(size_t)p * T.m + c] = make_float2((float)v.x, (float)v.y);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int rx = T.roles[3 * p + 0];
+  const double2* xr = xrow(T, rx, p);
+  const unsigned char* ox = T.occ + rx * (size_t)T.P * T.NT + (size_t)p * T.NT;
+  for (int t = blockIdx.y * nw + warp; t < T.NT; t += gridDim.y * nw) {
+    int b = 0;
+    while (b + 1 < T.J && T.ftile[b + 1] <= t) ++b;
+    const int cs = T.bstart[b] + (t - T.ftile[b]) * TL_CT, ce = min(T.bstart[b + 1], cs + TL_CT);
+    const bool f = ox[t] != 0;
+#pragma unroll
+    for (int h = 0; h < TL_CT / 32; ++h) {
+      const int c = cs + lane + 32 * h;
+      if (c < ce) {
+        const double2 v = f ? xr[c] : make_double2(0.0, 0.0);
+        T.X[(size_t)p * T.m + c] = make_float2((float)v.x, (float)v.y);
+      }
+    }
   }
   if (blockIdx.y == 0 && threadIdx.x == 0) {
     T.f_final[p] = T.F[p];
@@ -608,7 +665,7 @@ cudaError_t tiled_update(const TiledParams& T, cudaStream_t st) {
   int maxw = 0;
   // widest block (host copy of the starts is not kept here; bound by m / J rounded up)
   maxw = (T.m + T.J - 1) / T.J + 1;
-  int chunks = (maxw + 2047) / 2048;  // ~8 columns per thread
+  int chunks = (maxw / TL_CT + 31) / 32;  // 8 warps x ~4 occupancy tiles per CTA
   chunks = chunks < 1 ? 1 : chunks > 64 ? 64 : chunks;
   dim3 grid(T.P, chunks);
   count_launch();
@@ -617,7 +674,7 @@ cudaError_t tiled_update(const TiledParams& T, cudaStream_t st) {
 }
 
 cudaError_t tiled_finish(const TiledParams& T, cudaStream_t st) {
-  int chunks = (T.m + 2047) / 2048;
+  int chunks = (T.NT + 31) / 32;  // 8 warps x ~4 tiles per CTA
   chunks = chunks < 1 ? 1 : chunks > 64 ? 64 : chunks;
   dim3 grid(T.P, chunks);
   count_launch();

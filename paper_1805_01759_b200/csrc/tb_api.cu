@@ -381,6 +381,15 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   sz[ns++] = red_dev ? 0 : align256(sizeof(double) * P * (2 * n + 4));  // red + redsc
   sz[ns++] = align256(sizeof(double) * J * 2);           // alpha0, cdf
   sz[ns++] = align256(sizeof(int) * (J + 1));            // bstart
+  // occupancy tiles: TL_CT-column tiles cut per block from its first column
+  std::vector<int> hft(J + 1, 0);
+  for (int j = 0; j < J; ++j) {
+    const long long w = rb ? (long long)c->bstart_host[j + 1] - c->bstart_host[j] : m;
+    hft[j + 1] = hft[j] + (int)((w + tb::TL_CT - 1) / tb::TL_CT);
+  }
+  const int NT = hft[J];
+  sz[ns++] = align256((size_t)3 * P * NT);               // occ
+  sz[ns++] = align256(sizeof(int) * (J + 1));            // ftile
   // tensor-core adjoint: packed dictionary, packed r_y, G = A^H r_y, tile bases
   const bool tc = tiled_use_tc();
   std::vector<int> tc_base(J + 1, 0);
@@ -456,6 +465,10 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   T.alpha0 = tabs;
   T.cdf = tabs + J;
   T.bstart = bst;
+  T.occ = take(0);
+  int* ftl = (int*)take(0);
+  T.ftile = ftl;
+  T.NT = NT;
   if (tc) {
     h->Apk = (float*)take(0);
     h->Rpk = (float*)take(0);
@@ -510,8 +523,9 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   T.seeds = seeds;
   T.hist = hist;
   T.hist_stride = hist_stride;
-  // x = prev = 0 (solver.py:270-272, 348)
-  TB_CUDA(cudaMemsetAsync(T.X3, 0, sizeof(double2) * 2ull * P * m, st));
+  // x = prev = 0 (solver.py:270-272, 348): every state tile starts unoccupied (logically zero)
+  TB_CUDA(cudaMemsetAsync(T.occ, 0, (size_t)3 * P * NT, st));
+  TB_CUDA(cudaMemcpyAsync(ftl, hft.data(), sizeof(int) * (J + 1), cudaMemcpyHostToDevice, st));
   const int rem = (int)P;
   TB_CUDA(cudaMemcpyAsync(T.remaining, &rem, sizeof(int), cudaMemcpyHostToDevice, st));
   TB_CUDA(tb::tiled_init(T, st));

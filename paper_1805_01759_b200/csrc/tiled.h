@@ -35,6 +35,14 @@ struct TiledParams {
   const float* lam;      // [P]
   const uint64_t* seeds; // [P]
   double2* X3;           // 3 x [P][m] fp64 state buffers
+  // Tile occupancy of the state buffers: occ[buf][p][t] == 0 means TL_CT-column tile t of buffer
+  // buf of pixel p is all zero (its memory is then never read, and a zero candidate tile is never
+  // written).  Tiles are cut per block from its first column (ftile[b] = first tile of block b), so
+  // every pass column tile is exactly one occupancy tile.  L1 iterates are sparse after the first
+  // iterations, so this removes most of the fp64 state traffic.
+  unsigned char* occ;    // [3][P][NT]
+  const int* ftile;      // device [J+1]
+  int NT;
   // per-pixel state
   int* phase;
   int* k;
