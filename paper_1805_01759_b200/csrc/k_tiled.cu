@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
         for (int j = 0; j < 4; ++j)
           if (cg + 16 * j < ncols) acc[q][j] = g[cg + 16 * j];
       }
-    } else
+    } else if (2 * pg < count)  // pixel pairs past the tile's count (few-RHS RBPG rounds) skip the GEMM
     for (int i = 0; i < n; ++i) {
       const float4 r2 = *reinterpret_cast<const float4*>(&sRY[i * TL_PT + 2 * pg]);
       const float2 ra = make_float2(r2.x, r2.y), rbv = make_float2(r2.z, r2.w);
