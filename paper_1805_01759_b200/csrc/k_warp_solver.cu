@@ -104,17 +104,25 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
   __syncthreads();
   off += block_table_bytes(J);
   const double alpha0_full = P.alpha_scale / fmax(P.lip_full, 1e-300);  // solver.py:345
-  const size_t per_warp = warp_slot_bytes(n, m, P.max_width, J);
+  // DC (RBPG): the extrapolation memory d = x - prev lives in fp64 in global memory (L2-resident,
+  // one m-vector per warp slot) and delta_b = A_b d_b is cached per block in shared memory, so the
+  // reference's r_y = r + A_b dy (solver.py:290-291) is r + m_k delta_b (dy = m_k d_b) with no
+  // forward product, and delta_b is refreshed on accept from quantities already at hand:
+  // A_b (z_b - x_b) = A_b dz + m_k delta_b.
+  constexpr bool DC = RB && TB_WS_DCACHE;
+  const size_t per_warp = warp_slot_bytes_for(RB, n, m, P.max_width, J);
   unsigned char* wb = smem + off + (size_t)warp * per_warp;
   double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA)
   double2* apv = rv + n;                         // A x_prev (FISTA)
-  double2* xs = apv + n;                         // x (fp64 iterate)
+  double2* xs = DC ? rv + n : apv + n;           // x (fp64 iterate)
   double2* zs = xs + m;                          // broadcast buffer for forward products [max_width]
   float4* ryv = reinterpret_cast<float4*>(zs + P.max_width);  // r_y rounded, as (r.x, r.y, r.y, -r.x)
-  float2* ds = reinterpret_cast<float2*>(ryv + n);  // d = x - prev, fp32 (y = x + m_k d)
-  float2* bv = ds + m;                           // b
-  double* ring = reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
+  float2* ds = reinterpret_cast<float2*>(ryv + n);  // d = x - prev, fp32 (y = x + m_k d); not DC
+  float2* bv = ds + m;                           // b; not RBPG
+  double2* dlt = reinterpret_cast<double2*>(ryv + n);  // DC: delta [J][n]
+  double* ring = DC ? reinterpret_cast<double*>(dlt + (size_t)J * n) : reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
   double* l1blk = ring + 16;                     // RBPG: sum |x_b| per block (updated on accept)
+  double2* dg = DC ? P.dglob + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * m : nullptr;
 
   auto Aat = [&](int i, int c) -> float2 {
     if (ASMEM) return As[(size_t)i * ms + c];
@@ -173,14 +181,21 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     // ---- initial state: x = 0, prev = 0, r = -b, F0 = ||b||^2 (solver.py:270-276, 349)
     for (int c = lane; c < m; c += 32) {
       xs[c] = make_double2(0.0, 0.0);
-      ds[c] = make_float2(0.f, 0.f);
+      if (DC)
+        dg[c] = make_double2(0.0, 0.0);
+      else
+        ds[c] = make_float2(0.f, 0.f);
     }
+    if (DC)
+      for (int e = lane; e < J * n; e += 32) dlt[e] = make_double2(0.0, 0.0);
     double fb = 0.0;
     for (int i = lane; i < n; i += 32) {
       float2 b = P.B[(size_t)p * n + i];
-      bv[i] = b;
+      if (!RB) {
+        bv[i] = b;
+        apv[i] = make_double2(0.0, 0.0);
+      }
       rv[i] = RB ? make_double2(-(double)b.x, -(double)b.y) : make_double2(0.0, 0.0);
-      apv[i] = make_double2(0.0, 0.0);
       fb += (double)b.x * b.x + (double)b.y * b.y;
     }
     double F = warp_sum(fb);
@@ -242,8 +257,16 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       // Column passes are branch-free: lanes past the range read a valid column (cs) and their
       // results are masked, so no divergent-branch reconvergence is paid per pass; passes that lie
       // entirely past the range are skipped with a warp-uniform test.
+      // DC: the block's d_b is loaded from L2 here and first used in the backtracking loop, so the
+      // load latency hides behind the adjoint.
+      double2 dvb[DC ? MAXT : 1];
 #pragma unroll
-      for (int t = 0; t < MAXT; ++t) {
+      for (int t = 0; t < (DC ? MAXT : 1); ++t) {
+        dvb[t] = make_double2(0.0, 0.0);
+        if (DC && (t == 0 || 32 * t < width)) dvb[t] = dg[cs + min(lane + 32 * t, width - 1)];
+      }
+#pragma unroll
+      for (int t = 0; t < (DC ? 0 : MAXT); ++t) {
         masks[t] = 0u;
         if (t > 0 && 32 * t >= width) continue;
         const int cl = lane + 32 * t;
@@ -278,7 +301,20 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       // ---- residual at y (lane = row), fp64: RBPG r_y = r + A_b dy (solver.py:290-291);
       //      FISTA/ISTA r_y = A y - b with A y = A x + m_k (A x - A x_prev) by linearity.
       double2 ry[MAXQ], ay[MAXQ];
-      if (RB) {
+      if (DC) {
+        // r_y = r + m_k delta_b: delta_b = 0 after a rejected (or no) visit gives r exactly, as the
+        // reference's `np.any(dy)` test does
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          const int i = lane + 32 * q;
+          ry[q] = ay[q] = make_double2(0.0, 0.0);
+          if (i < n) {
+            const double2 r = rv[i], dl = dlt[blk * n + i];
+            ry[q] = make_double2(fma(mk, dl.x, r.x), fma(mk, dl.y, r.y));
+            ryv[i] = conj_operand((float)ry[q].x, (float)ry[q].y);
+          }
+        }
+      } else if (RB) {
         double2 acc[MAXQ];
         if (any_dy) forward_list(clist, cnt, acc);
 #pragma unroll
@@ -344,7 +380,10 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           // y = x + m_k d recomputed from shared memory (keeps registers for occupancy)
           const double2 xv = xs[col];
           double2 yv = xv;
-          if (!ista) {
+          if (DC) {
+            yv.x = fma(mk, dvb[t].x, xv.x);
+            yv.y = fma(mk, dvb[t].y, xv.y);
+          } else if (!ista) {
             const float2 dv = ds[col];
             yv.x = fma(mk, (double)dv.x, xv.x);
             yv.y = fma(mk, (double)dv.y, xv.y);
@@ -451,8 +490,23 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           if (cl < width) {
             // accept: prev_b <- x_b, x_b <- z_b; reject: prev_b <- x_b (solver.py:318-325)
             const double2 xv = xs[cs + cl], zv = accept ? z[RB ? t : 0] : xv;
-            ds[cs + cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
+            if (DC)
+              dg[cs + cl] = make_double2(zv.x - xv.x, zv.y - xv.y);
+            else
+              ds[cs + cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
             xs[cs + cl] = zv;
+          }
+        }
+        if (DC) {
+          // delta_b <- A_b (z_b - x_b) = A_b dz + A_b (y_b - x_b) = adz + m_k delta_b, or 0 on reject
+#pragma unroll
+          for (int q = 0; q < MAXQ; ++q) {
+            const int i = lane + 32 * q;
+            if (i < n) {
+              double2* dl = dlt + blk * n + i;
+              const double2 o = *dl;
+              *dl = accept ? make_double2(fma(mk, o.x, adz[q].x), fma(mk, o.y, adz[q].y)) : make_double2(0.0, 0.0);
+            }
           }
         }
         if (accept) {
@@ -565,7 +619,7 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   int maxq = (P.n + 31) / 32;
   maxq = maxq <= 1 ? 1 : maxq <= 2 ? 2 : 4;
   const int J = P.mode == SOLVER_RBPG ? P.num_blocks : 1;
-  const size_t slot = warp_slot_bytes(P.n, P.m, P.max_width, J);
+  const size_t slot = warp_slot_bytes_for(P.mode == SOLVER_RBPG, P.n, P.m, P.max_width, J);
   const size_t tables = block_table_bytes(J);
   const size_t a_bytes = ((size_t)P.n * P.ms * sizeof(float2) + 15) & ~(size_t)15;
   const size_t cap = 227 * 1024;

@@ -35,7 +35,14 @@ struct SolveParams {
   int* iters;
   int* status;
   unsigned long long* queue;
+  double2* dglob;  // RBPG (TB_WS_DCACHE): fp64 extrapolation memory d = x - prev, [slots][m], L2-resident
 };
+
+// RBPG keeps d = x - prev in fp64 in global memory (L2) and caches delta_b = A_b d_b per block in
+// shared memory, so r_y = r + m_k delta_b needs no forward product (see k_warp_solver.cu).
+#ifndef TB_WS_DCACHE
+#define TB_WS_DCACHE 1
+#endif
 
 // per-warp shared bytes: 2 fp64 n-vectors, fp64 x (m) + fp64 broadcast buffer (width), fp32 d = x - prev
 // (m), fp32 r_y as float4 + fp32 b (n each), 16-double ring, J-double per-block l1 cache, 32 buffered
@@ -43,6 +50,15 @@ struct SolveParams {
 __host__ __device__ inline size_t warp_slot_bytes(int n, int m, int width, int J) {
   size_t b = (size_t)n * 32 + (size_t)(m + width) * 16 + (size_t)m * 8 + (size_t)n * 24 + 16 * 8 + (size_t)J * 8 + 32 * 8 + (size_t)width * 4;
   return (b + 15) & ~(size_t)15;
+}
+// RBPG slot with the delta cache: fp64 r, fp64 x (m), fp64 broadcast buffer (width), r_y quads (n),
+// delta_b = A_b d_b for every block (J x n fp64), ring, per-block l1, Philox buffer, column list
+__host__ __device__ inline size_t warp_slot_bytes_dc(int n, int m, int width, int J) {
+  size_t b = (size_t)n * 16 + (size_t)m * 16 + (size_t)width * 16 + (size_t)n * 16 + (size_t)J * n * 16 + 16 * 8 + (size_t)J * 8 + 32 * 8 + (size_t)width * 4;
+  return (b + 15) & ~(size_t)15;
+}
+__host__ __device__ inline size_t warp_slot_bytes_for(bool rb, int n, int m, int width, int J) {
+  return (rb && TB_WS_DCACHE) ? warp_slot_bytes_dc(n, m, width, J) : warp_slot_bytes(n, m, width, J);
 }
 // per-CTA block tables: cdf, alpha0 (J doubles each) + J+1 block starts
 __host__ __device__ inline size_t block_table_bytes(int J) {

@@ -37,6 +37,9 @@ struct tb_ctx {
   unsigned char* ws = nullptr;
   size_t ws_size = 0;
   bool ws_busy = false;
+  // warp solver RBPG extrapolation memory (fp64 d per warp slot), grow-only
+  double2* dglob = nullptr;
+  size_t dglob_elems = 0;
 };
 
 struct tb_tiled {
@@ -144,6 +147,7 @@ int tb_ctx_destroy(tb_ctx* c) {
   cudaFree(c->queue);
   cudaFree(c->mk);
   cudaFree(c->ws);
+  cudaFree(c->dglob);
   delete c;
   return TB_OK;
 }
@@ -331,7 +335,7 @@ static bool warp_path_fits(tb_ctx* c, int32_t solver) {
   const int width = solver == TB_SOLVER_RBPG ? c->max_block_width : (int)c->m;
   if ((width + 31) / 32 > 16) return false;
   const int J = solver == TB_SOLVER_RBPG ? c->num_blocks : 1;
-  const size_t slot = tb::warp_slot_bytes((int)c->n, (int)c->m, width, J);
+  const size_t slot = tb::warp_slot_bytes_for(solver == TB_SOLVER_RBPG, (int)c->n, (int)c->m, width, J);
   return tb::block_table_bytes(J) + 4 * slot <= 227 * 1024;
 }
 
@@ -670,6 +674,18 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   S.status = status;
   S.queue = c->queue;
   S.mk = c->mk;
+  if (solver == TB_SOLVER_RBPG && TB_WS_DCACHE) {
+    const size_t need = (size_t)c->num_sms * 32 * (size_t)c->m;  // >= resident warp slots x m
+    if (c->dglob_elems < need) {
+      TB_CUDA(cudaStreamSynchronize(st));
+      cudaFree(c->dglob);
+      c->dglob = nullptr;
+      c->dglob_elems = 0;
+      TB_CUDA(cudaMalloc((void**)&c->dglob, sizeof(double2) * need));
+      c->dglob_elems = need;
+    }
+    S.dglob = c->dglob;
+  }
   TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
   const char* force = getenv("TB_RBPG_KERNEL");
   // the half-warp-per-pixel RBPG variant measured slower on cfg2 (0.68 vs 1.07 M px/s); opt-in only
