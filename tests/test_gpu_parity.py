@@ -241,3 +241,24 @@ def test_svd_wiener_backend(tb, golden, cfg1, mu):
     assert np.array_equal(est.model_order.cpu().numpy(), golden[f"wiener{mu}/order"])
     obj = tb.Objective(dictionary=golden["cfg1/a"].astype(np.complex128), measurement=pix[0], lambda_reg=0.0)
     np.testing.assert_allclose(tb.svd_wiener_solve(obj, mu), ref[0], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("num_blocks", [1, 5, 13, 40])
+def test_rbpg_block_counts_vs_oracle(tb, num_blocks):
+    """RBPG with block counts other than the default 8 (the per-block delta cache, the block
+    table and the column-pass dispatch all depend on J): iterations and statuses identical to the
+    oracle, objective within 1e-6."""
+    from paper_1805_01759_b200.synth import make_config
+
+    batch = make_config(1, num_pixels=48)
+    d = tb.Dictionary(batch.dictionary)
+    lam = d.default_lambda(batch.pixels, 0.1)
+    seeds = d.derive_seeds(2018, 48)
+    cfg = tb.SolverConfig(max_iters=300, tol=1e-6, num_blocks=num_blocks)
+    r = d.solve(batch.pixels, lam, cfg, "rbpg", seeds=seeds)
+    lips = d.partition(num_blocks).lipschitz
+    ref = OB.run(batch.dictionary.astype(np.complex128), batch.pixels, lam.cpu().numpy(), "rbpg", seeds=seeds.cpu().numpy(),
+                 lips=lips, max_iters=300, tol=1e-6, num_blocks=num_blocks)
+    assert np.array_equal(r.iterations.cpu().numpy(), np.array([x["iterations"] for x in ref]))
+    assert np.array_equal(r.status.cpu().numpy(), np.array([O.STATUS_CODES[x["status"]] if isinstance(x["status"], str) else x["status"] for x in ref]))
+    np.testing.assert_allclose(r.objective_final.cpu().numpy(), np.array([x["f_final"] for x in ref]), rtol=1e-6)
