@@ -27,6 +27,9 @@
 #ifndef TB_WS_RSQRT
 #define TB_WS_RSQRT 1  // soft threshold from one fp64 rsqrt
 #endif
+#ifndef TB_WS_COLMAJOR
+#define TB_WS_COLMAJOR 1  // RBPG: shared-memory dictionary column-major (odd column stride n | 1)
+#endif
 #ifndef TB_WARP_LB_WIDE
 #define TB_WARP_LB_WIDE 384
 #endif
@@ -39,36 +42,39 @@ namespace tb {
 // acc[t] += conj(A[i][c + 32 t]) r_y[i] over all n rows for NP column passes (lane = column; only the
 // last pass can be partial: `last` = lane + 32 (NP - 1) < width), rows unrolled by 8 (loop and
 // address overhead once per 8 rows), fp32 packed FFMA2 sharing each broadcast r_y load.
-template <int NP, bool ASMEM>
-__device__ __forceinline__ void adjoint_passes(float2* acc, const float2* ap, int stride, const float4* ryv, int n, bool last) {
+// Element (row i, pass t) lives at ap[i rs + t ps]: shared memory column-major (rs = 1, so the 8
+// unrolled rows are immediate offsets; ps = 32 column strides) or global row-major (rs = m, ps = 32).
+template <int NP, bool ASMEM, bool CM>
+__device__ __forceinline__ void adjoint_passes(float2* acc, const float2* ap, int stride, int pstride, const float4* ryv, int n, bool last) {
+  const int rs = CM ? 1 : stride;
   int i = 0;
 #pragma unroll 1
-  for (; i + 8 <= n; i += 8, ap += 8 * stride) {
+  for (; i + 8 <= n; i += 8, ap += 8 * rs) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const float4 r = ryv[i + u];
 #pragma unroll
       for (int t = 0; t < NP; ++t)
-        if (t < NP - 1 || last) cfma_conj_x2(acc[t], ASMEM ? ap[u * stride + 32 * t] : __ldg(ap + u * stride + 32 * t), r);
+        if (t < NP - 1 || last) cfma_conj_x2(acc[t], ASMEM ? ap[u * rs + t * pstride] : __ldg(ap + u * rs + t * pstride), r);
     }
   }
 #pragma unroll 1
-  for (; i < n; ++i, ap += stride) {
+  for (; i < n; ++i, ap += rs) {
     const float4 r = ryv[i];
 #pragma unroll
     for (int t = 0; t < NP; ++t)
-      if (t < NP - 1 || last) cfma_conj_x2(acc[t], ASMEM ? ap[32 * t] : __ldg(ap + 32 * t), r);
+      if (t < NP - 1 || last) cfma_conj_x2(acc[t], ASMEM ? ap[t * pstride] : __ldg(ap + t * pstride), r);
   }
 }
 // runtime pass count -> compile-time unrolled body (no all-idle passes are issued)
-template <int NP, int MAXT, bool ASMEM>
-__device__ __forceinline__ void adjoint_dispatch(int passes, float2* acc, const float2* ap, int stride, const float4* ryv, int n, bool last) {
+template <int NP, int MAXT, bool ASMEM, bool CM>
+__device__ __forceinline__ void adjoint_dispatch(int passes, float2* acc, const float2* ap, int stride, int pstride, const float4* ryv, int n, bool last) {
   if constexpr (NP <= MAXT) {
     if (passes == NP) {
-      adjoint_passes<NP, ASMEM>(acc, ap, stride, ryv, n, last);
+      adjoint_passes<NP, ASMEM, CM>(acc, ap, stride, pstride, ryv, n, last);
       return;
     }
-    adjoint_dispatch<NP + 1, MAXT, ASMEM>(passes, acc, ap, stride, ryv, n, last);
+    adjoint_dispatch<NP + 1, MAXT, ASMEM, CM>(passes, acc, ap, stride, pstride, ryv, n, last);
   }
 }
 
@@ -78,14 +84,19 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int n = P.n, m = P.m, ms = P.ms;
+  constexpr bool CM = ASMEM && RB && TB_WS_COLMAJOR;  // measured: +0.6% RBPG, -2% FISTA (cfg2)
+  const int ns = n | 1;  // odd column stride of the column-major shared dictionary
   const bool ista = P.mode == SOLVER_ISTA;
 
   float2* As = reinterpret_cast<float2*>(smem);
-  size_t off = ASMEM ? (((size_t)n * ms * sizeof(float2) + 15) & ~(size_t)15) : 0;
+  size_t off = ASMEM ? ((((size_t)(CM ? (size_t)m * ns : (size_t)n * ms)) * sizeof(float2) + 15) & ~(size_t)15) : 0;
   if (ASMEM) {
     for (int idx = threadIdx.x; idx < n * m; idx += blockDim.x) {
       int i = idx / m, c = idx - i * m;
-      As[(size_t)i * ms + c] = __ldg(&P.A[idx]);
+      if (CM)
+        As[(size_t)c * ns + i] = __ldg(&P.A[idx]);
+      else
+        As[(size_t)i * ms + c] = __ldg(&P.A[idx]);
     }
     __syncthreads();
   }
@@ -124,10 +135,6 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
   double* l1blk = ring + 16;                     // RBPG: sum |x_b| per block (updated on accept)
   double2* dg = DC ? P.dglob + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * m : nullptr;
 
-  auto Aat = [&](int i, int c) -> float2 {
-    if (ASMEM) return As[(size_t)i * ms + c];
-    return __ldg(&P.A[(size_t)i * m + c]);
-  };
   // acc[q] += sum over the nonzero entries of the step (lane = row), fp64 accumulation.  L1 iterates
   // and their steps are sparse: the lanes compact the nonzero entries with __ballot_sync into
   // zs[0..cnt) in ascending column order, their dictionary columns in clist, and only those
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     for (int q = 0; q < MAXQ; ++q) {
       acc[q] = make_double2(0.0, 0.0);
       const int i = min(lane + 32 * q, n - 1);
-      arow[q] = ASMEM ? As + i * ms : P.A + (size_t)i * m;
+      arow[q] = CM ? As + i : ASMEM ? As + i * ms : P.A + (size_t)i * m;  // CM: cl holds column * ns
     }
     int e = 0;
     for (; e + 2 <= cnt; e += 2) {
@@ -291,7 +298,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         if (RB && nz) {
           const int pos = cnt + __popc(masks[t] & lt_mask);
           zs[pos] = dyv;
-          clist[pos] = col;
+          clist[pos] = CM ? col * ns : col;
         }
         cnt += __popc(masks[t]);
         any_dy |= masks[t] != 0u;
@@ -355,7 +362,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
         const int passes = (width + 31) >> 5;
-        adjoint_dispatch<1, MAXT, ASMEM>(passes, acc, (ASMEM ? As : P.A) + cs + lane, ASMEM ? ms : m, ryv, n, lane + 32 * (passes - 1) < width);
+        adjoint_dispatch<1, MAXT, ASMEM, CM>(passes, acc, CM ? As + (size_t)(cs + lane) * ns : (ASMEM ? As : P.A) + cs + lane, ASMEM ? ms : m,
+                                         CM ? 32 * ns : 32, ryv, n, lane + 32 * (passes - 1) < width);
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) g[t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
       }
@@ -414,7 +422,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           if (nz) {
             const int pos = cnt + __popc(masks[t] & lt_mask);
             zs[pos] = dw;
-            clist[pos] = col;
+            clist[pos] = CM ? col * ns : col;
           }
           cnt += __popc(masks[t]);
         }
@@ -621,7 +629,8 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   const int J = P.mode == SOLVER_RBPG ? P.num_blocks : 1;
   const size_t slot = warp_slot_bytes_for(P.mode == SOLVER_RBPG, P.n, P.m, P.max_width, J);
   const size_t tables = block_table_bytes(J);
-  const size_t a_bytes = ((size_t)P.n * P.ms * sizeof(float2) + 15) & ~(size_t)15;
+  const bool cm = TB_WS_COLMAJOR && P.mode == SOLVER_RBPG;
+  const size_t a_bytes = ((size_t)(cm ? (size_t)P.m * (P.n | 1) : (size_t)P.n * P.ms) * sizeof(float2) + 15) & ~(size_t)15;
   const size_t cap = 227 * 1024;
   const int max_warps = maxt >= 8 ? TB_WARP_LB_WIDE / 32 : TB_WARP_LB / 32;
   bool asmem = a_bytes + tables + 4 * slot <= cap;
