@@ -643,6 +643,10 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
     const int cap_l1 = ev ? atoi(ev) : warps;
     if (cap_l1 >= 1 && cap_l1 < warps) warps = cap_l1;
   }
+  if (const char* wc = getenv("TB_WARPS_CAP")) {  // tuning/diagnostics: cap the warps per CTA
+    const int cap_w = atoi(wc);
+    if (cap_w >= 1 && cap_w < warps) warps = cap_w;
+  }
   if (warps < 1) return cudaErrorInvalidValue;
   size_t smem = (asmem ? a_bytes : 0) + tables + (size_t)warps * slot;
   long long need = (P.num_pixels + warps - 1) / warps;
