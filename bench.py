@@ -88,12 +88,16 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):  # diagnostics only: the line then reports no clocks
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
             )
-            time.sleep(0.5)  # let nvidia-smi start up before the timed region (its start-up competes with launches)
+            # wait for the first sample: nvidia-smi's start-up (NVML init) stalls kernel launches, so
+            # it must not overlap a short timed region
+            self.first = self.proc.stdout.readline()
         except Exception:
             self.proc = None
 
@@ -103,11 +107,17 @@ class ClockSampler:
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
         rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 6]
+        pre = not rows  # region shorter than one sampling period: report the sample taken just before it
+        if pre:
+            rows = [r.split(",") for r in getattr(self, "first", "").strip().splitlines() if r.count(",") >= 6]
         sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[j] for r in rows for j in range(4) if r[3 + j].strip().lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+        res = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+        if pre:
+            res["note"] = "timed region shorter than the 200 ms sampling period; sample taken just before it"
+        return res
 
 
 def fp32_peak():
@@ -208,9 +218,8 @@ def run_b200(args):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    ks, ke = [], []
+    ks, ke, its_list = [], [], []
     launches0 = tb._lib.launch_count()
-    iters_total = 0
     ev0.record(stream)
     for _ in range(args.steps):
         lam = d.default_lambda(pix_dev, 0.1)
@@ -223,7 +232,7 @@ def run_b200(args):
         est = tb.select_batch(d, sol.x_hat, pix_dev, grid, batch.k_max)
         ks.append(a)
         ke.append(b)
-        iters_total += sol.iterations  # device tensor accumulate (no sync)
+        its_list.append(sol.iterations)  # summed after the timed region (no torch kernel inside it)
     ev1.record(stream)
     launches = tb._lib.launch_count() - launches0
     torch.cuda.synchronize()
@@ -232,7 +241,7 @@ def run_b200(args):
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     kms = [x.elapsed_time(y) for x, y in zip(ks, ke)]
-    pix_iters = float(iters_total.double().sum().item()) if hasattr(iters_total, "double") else 0.0
+    pix_iters = float(sum(float(x.double().sum().item()) for x in its_list))
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
