@@ -359,13 +359,18 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   const int maxw = rb ? c->max_block_width : (int)m;
   // split width: the pass grid (pixel tiles x splits) should fill whole waves of 2 CTAs/SM: the
   // CTAs are long (each walks its split's column tiles), so a 5th wave that is 10% full costs
-  // nearly a whole wave.  Splits = floor(4 waves / tiles) (TB_TILED_SPLITS=ceil restores the
-  // former ceil rule, for A/B); RBPG rounds have ~P/32 + J/2 tiles (partial tile per block).
+  // nearly a whole wave.  Splits = floor(waves / tiles) (TB_TILED_SPLITS=ceil restores the former
+  // 4-wave ceil rule, TB_TILED_WAVES overrides the wave count, for A/B); RBPG rounds have
+  // ~P/32 + J/2 tiles (a partial tile per block).
   const long long tiles = (P + tb::TL_PT - 1) / tb::TL_PT + (rb ? J : 0);
   const long long tiles_eff = (P + tb::TL_PT - 1) / tb::TL_PT + (rb ? (J + 1) / 2 : 0);
   const char* sm_env = getenv("TB_TILED_SPLITS");
   const bool ceil_rule = sm_env && strcmp(sm_env, "ceil") == 0;
-  long long s_target = ceil_rule ? (4ll * 2 * c->num_sms + tiles - 1) / tiles : (4ll * 2 * c->num_sms) / tiles_eff;
+  const char* wv_env = getenv("TB_TILED_WAVES");
+  // many pixel tiles (cfg4): 8 shorter waves balance the uneven (sparsity-dependent) CTA work;
+  // few tiles (cfg5's 64 RHS): 4 waves, since every extra split adds a [P][n] partial to reduce
+  const long long waves = wv_env && atoi(wv_env) > 0 ? atoi(wv_env) : (tiles_eff >= 16 ? 8 : 4);
+  long long s_target = ceil_rule ? (4ll * 2 * c->num_sms + tiles - 1) / tiles : (waves * 2 * c->num_sms) / tiles_eff;
   if (s_target < 1) s_target = 1;
   long long sw = (maxw + s_target - 1) / s_target;
   sw = ((sw + tb::TL_CT - 1) / tb::TL_CT) * tb::TL_CT;
