@@ -221,6 +221,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     bool stopped = false;
     __syncwarp();
 
+    // m_k is read one iteration ahead: the table load (L1 or L2) is off the r_y critical path
+    double mk_next = (ista || P.total_iters < 1) ? 0.0 : __ldg(P.mk + 1);
     for (int k = 1; k <= P.total_iters; ++k) {
       iters = k;
       ridx = ridx == STOP_WINDOW ? 0 : ridx + 1;
@@ -253,7 +255,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         ce = s_bstart[blk + 1];
       }
       const int width = ce - cs;
-      const double mk = ista ? 0.0 : P.mk[k];  // (k-2)/(k+1), host table (solver.py:222-224)
+      const double mk = mk_next;  // (k-2)/(k+1), host table (solver.py:222-224); 0 for ISTA
+      if (!ista && k < P.total_iters) mk_next = __ldg(P.mk + k + 1);
 
       // ---- extrapolation y = x + m_k (x - prev) (solver.py:288-289, 356)
       float2 g[MAXT];
