@@ -30,6 +30,9 @@
 #ifndef TB_WS_COLMAJOR
 #define TB_WS_COLMAJOR 1  // RBPG: shared-memory dictionary column-major (odd column stride n | 1)
 #endif
+#ifndef TB_WS_BLKBUF
+#define TB_WS_BLKBUF 1  // block indices for 32 draws computed at the Philox refill (+2% cfg2 RBPG)
+#endif
 #ifndef TB_WARP_LB_WIDE
 #define TB_WARP_LB_WIDE 384
 #endif
@@ -232,6 +235,28 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         // raw draw k-1 of Philox(key=[seed, 0]): counter (k-1)/4 + 1, output (k-1) % 4.  Every 32
         // draws, lanes 0..7 evaluate the next 8 counters in parallel into the slot's buffer.
         const int w = (k - 1) & 31;
+#if TB_WS_BLKBUF
+        // every 32 draws: lanes 0..7 evaluate 8 counters, then lane l turns draw l into its block
+        // (searchsorted(cdf, u, 'right') as a linear scan of the monotone CDF) and the 32 block
+        // indices replace the raw draws in the slot's buffer
+        int* bbuf = reinterpret_cast<int*>(rbuf);
+        if (w == 0) {
+          uint64_t c4[4] = {(uint64_t)((k - 1) >> 2) + 1ull + (uint64_t)(lane & 7), 0ull, 0ull, 0ull};
+          philox4x64_10(c4, seed, 0ull);
+          if (lane < 8) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rbuf[4 * lane + q] = c4[q];
+          }
+          __syncwarp();
+          const double u = raw_to_unit(rbuf[lane]);
+          int j = 0;
+          while (j < J - 1 && s_cdf[j] <= u) ++j;
+          __syncwarp();
+          bbuf[lane] = j;
+          __syncwarp();
+        }
+        blk = bbuf[w];
+#else
         if (w == 0) {
           uint64_t c4[4] = {(uint64_t)((k - 1) >> 2) + 1ull + (uint64_t)(lane & 7), 0ull, 0ull, 0ull};
           philox4x64_10(c4, seed, 0ull);
@@ -251,6 +276,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           while (j < J - 1 && s_cdf[j] <= u) ++j;
         }
         blk = j;
+#endif
         cs = s_bstart[blk];
         ce = s_bstart[blk + 1];
       }
