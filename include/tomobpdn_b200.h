@@ -99,7 +99,9 @@ int tb_derive_seeds(uint64_t run_seed, int64_t first_pixel_id, int64_t num_pixel
  *  may be NULL otherwise);  x_dev complex64 [P, m] out (Solution.x_hat);
  *  f_final_dev double [P] out (objective_history[-1]);  history_dev double [P, hist_stride]
  *  out or NULL (objective_history, NaN-padded after iterations+1 entries);
- *  iterations_dev int32 [P] out;  status_dev int32 [P] out (TB_STATUS_*). */
+ *  iterations_dev int32 [P] out;  status_dev int32 [P] out (TB_STATUS_*).
+ *  Asynchronous on `stream`; not re-entrant per context (the context owns the solver workspace:
+ *  the RBPG extrapolation memory of the on-chip solver and the tiled solver's state buffers). */
 int tb_solve(tb_ctx* ctx, int32_t solver, const tb_solver_config* cfg, const void* pixels_dev,
              const float* lambda_dev, const uint64_t* seeds_dev, int64_t num_pixels, void* x_dev,
              double* f_final_dev, double* history_dev, int64_t hist_stride,
