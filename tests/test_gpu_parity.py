@@ -262,3 +262,34 @@ def test_rbpg_block_counts_vs_oracle(tb, num_blocks):
     assert np.array_equal(r.iterations.cpu().numpy(), np.array([x["iterations"] for x in ref]))
     assert np.array_equal(r.status.cpu().numpy(), np.array([O.STATUS_CODES[x["status"]] if isinstance(x["status"], str) else x["status"] for x in ref]))
     np.testing.assert_allclose(r.objective_final.cpu().numpy(), np.array([x["f_final"] for x in ref]), rtol=1e-6)
+
+
+def test_full_size_cfg2_sampled_vs_oracle(tb):
+    """The BASELINE cfg2 batch at full size (1,048,576 pixels, RBPG, the bench's settings): 192
+    pixels sampled across the whole batch (including the last ones, whose seeds come from large
+    pixel ids) match the oracle exactly in iterations, status and support, objective within 1e-6."""
+    from paper_1805_01759_b200.synth import make_config
+
+    batch = make_config(2)
+    d = tb.Dictionary(batch.dictionary)
+    pc = tb.PipelineConfig(solver=tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8, seed=2018), backend="rbpg", k_max=batch.k_max)
+    est = tb.pipeline_batch(d, batch.pixels, batch.grid, pc, beta=0.1)
+    rng = np.random.default_rng(7)
+    idx = np.sort(np.concatenate([rng.choice(batch.num_pixels, 184, replace=False), np.arange(batch.num_pixels - 8, batch.num_pixels)]))
+    idx = np.unique(idx)
+    lam = est.lam.cpu().numpy()[idx]
+    seeds = np.array([O.derive_seed(2018, int(p)) for p in idx], dtype=np.uint64)
+    grid = OB.GridDesc(batch.grid.elevation, batch.grid.motion_axes)
+    lips = d.partition(8).lipschitz
+    ref = OB.run(batch.dictionary.astype(np.complex128), batch.pixels[idx], lam, "rbpg", seeds=seeds, grid=grid, k_max=batch.k_max,
+                 lips=lips, max_iters=500, tol=1e-6, num_blocks=8)
+    its = est.solution.iterations.cpu().numpy()[idx]
+    st = est.solution.status.cpu().numpy()[idx]
+    ff = est.solution.objective_final.cpu().numpy()[idx]
+    sup = est.support.cpu().numpy()[idx]
+    order = est.model_order.cpu().numpy()[idx]
+    assert np.array_equal(its, np.array([r["iterations"] for r in ref]))
+    assert np.array_equal(st, np.array([O.STATUS_CODES[r["status"]] if isinstance(r["status"], str) else r["status"] for r in ref]))
+    np.testing.assert_allclose(ff, np.array([r["f_final"] for r in ref]), rtol=1e-6)
+    for k in range(len(idx)):
+        assert list(sup[k, : order[k]]) == list(ref[k]["support"]), (int(idx[k]), sup[k], ref[k]["support"])
