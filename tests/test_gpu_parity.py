@@ -293,3 +293,27 @@ def test_full_size_cfg2_sampled_vs_oracle(tb):
     np.testing.assert_allclose(ff, np.array([r["f_final"] for r in ref]), rtol=1e-6)
     for k in range(len(idx)):
         assert list(sup[k, : order[k]]) == list(ref[k]["support"]), (int(idx[k]), sup[k], ref[k]["support"])
+
+
+@pytest.mark.parametrize("cfg_id,backend", [(3, "rbpg"), (2, "fista"), (3, "fista")])
+def test_full_size_sampled_vs_oracle(tb, cfg_id, backend):
+    """Full-size BASELINE batches (cfg2 1,048,576 px / cfg3 262,144 px) solved on the GPU; 96
+    pixels sampled across the batch match the oracle in iterations, status and support."""
+    from paper_1805_01759_b200.synth import make_config
+
+    batch = make_config(cfg_id)
+    d = tb.Dictionary(batch.dictionary)
+    pc = tb.PipelineConfig(solver=tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8, seed=2018), backend=backend, k_max=batch.k_max)
+    est = tb.pipeline_batch(d, batch.pixels, batch.grid, pc, beta=0.1)
+    idx = np.unique(np.random.default_rng(cfg_id).choice(batch.num_pixels, 96, replace=False))
+    lam = est.lam.cpu().numpy()[idx]
+    seeds = np.array([O.derive_seed(2018, int(p)) for p in idx], dtype=np.uint64)
+    grid = OB.GridDesc(batch.grid.elevation, batch.grid.motion_axes)
+    lips = d.partition(8).lipschitz if backend == "rbpg" else d.lipschitz()
+    ref = OB.run(batch.dictionary.astype(np.complex128), batch.pixels[idx], lam, backend, seeds=seeds, grid=grid, k_max=batch.k_max,
+                 lips=lips, max_iters=500, tol=1e-6, num_blocks=8)
+    assert np.array_equal(est.solution.iterations.cpu().numpy()[idx], np.array([r["iterations"] for r in ref]))
+    np.testing.assert_allclose(est.solution.objective_final.cpu().numpy()[idx], np.array([r["f_final"] for r in ref]), rtol=1e-6)
+    sup, order = est.support.cpu().numpy()[idx], est.model_order.cpu().numpy()[idx]
+    for k in range(len(idx)):
+        assert list(sup[k, : order[k]]) == list(ref[k]["support"]), (int(idx[k]), sup[k], ref[k]["support"])
