@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(128) select_kernel(const SelectParams S) {
   double* prof = reinterpret_cast<double*>(base);
   int* amx = reinterpret_cast<int*>(prof + ne);
   double2* Q = reinterpret_cast<double2*>(base + (((size_t)ne * 12 + 15) & ~(size_t)15));  // [kmax][n]
+  double2* Rs = Q + (size_t)kmax * n;  // R[kmax][kmax], row-major, warp-uniform values
+#define R(r, c) Rs[(r) * kmax + (c)]
 
   for (long long p = (long long)blockIdx.x * nw + warp; p < S.num_pixels; p += (long long)gridDim.x * nw) {
     const float2* x = S.X + (size_t)p * m;
@@ -106,7 +108,6 @@ __global__ void __launch_bounds__(128) select_kernel(const SelectParams S) {
     gg = warp_sum(gg);
 
     // ---- rank filter via incremental MGS QR (slimmer.py:116-123)
-    double2 R[SEL_MAXK][SEL_MAXK];
     long long usable[SEL_MAXK];
     int nu = 0;
     double fro2 = 0.0;
@@ -166,8 +167,8 @@ __global__ void __launch_bounds__(128) select_kernel(const SelectParams S) {
           int i = lane + 32 * q;
           if (i < n) Q[(size_t)nu * n + i] = make_double2(a[q].x * inv, a[q].y * inv);
         }
-        for (int j = 0; j < SEL_MAXK; ++j) R[j][nu] = (j < nu) ? rcol[j] : make_double2(0.0, 0.0);
-        R[nu][nu] = make_double2(rn, 0.0);
+        for (int j = 0; j < nu; ++j) R(j, nu) = rcol[j];  // every lane stores the same value
+        R(nu, nu) = make_double2(rn, 0.0);
         usable[nu] = col;
         ++nu;
         fro2 += an;
@@ -222,11 +223,11 @@ __global__ void __launch_bounds__(128) select_kernel(const SelectParams S) {
     for (int r = khat - 1; r >= 0; --r) {
       double2 s = tq[r];
       for (int c = r + 1; c < khat; ++c) {
-        double2 rr = R[r][c], cc = coef[c];
+        double2 rr = R(r, c), cc = coef[c];
         s.x -= rr.x * cc.x - rr.y * cc.y;
         s.y -= rr.x * cc.y + rr.y * cc.x;
       }
-      double d = R[r][r].x;
+      double d = R(r, r).x;
       coef[r] = make_double2(s.x / d, s.y / d);
     }
 
@@ -260,6 +261,8 @@ __global__ void __launch_bounds__(128) select_kernel(const SelectParams S) {
     __syncwarp();
   }
 }
+
+#undef R
 
 cudaError_t launch_select(const SelectParams& S, int num_sms, cudaStream_t st) {
   if (S.num_pixels <= 0) return cudaSuccess;

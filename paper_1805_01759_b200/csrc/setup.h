@@ -41,10 +41,11 @@ struct SelectParams {
   int* err;
 };
 
-// per-warp shared bytes of the selection kernel: profile (double) + argmax (int) + Q[kmax][n]
+// per-warp shared bytes of the selection kernel: profile (double) + argmax (int) + Q[kmax][n] +
+// the triangular factor R[kmax][kmax] (warp-uniform values: shared, not per-lane local memory)
 __host__ __device__ inline size_t select_warp_bytes(int n, int n_elev, int kmax) {
   size_t a = ((size_t)n_elev * 12 + 15) & ~(size_t)15;
-  return a + (size_t)kmax * n * 16;
+  return a + (size_t)kmax * n * 16 + (size_t)kmax * kmax * 16;
 }
 
 cudaError_t launch_select(const SelectParams& S, int num_sms, cudaStream_t st);
