@@ -667,9 +667,11 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   int warps = (int)(avail / slot);
   if (warps > max_warps) warps = max_warps;
   if (!asmem) {
-    // dictionary read through L1/L2: leave part of the unified L1 for A (TB_WARPS_L1 overrides)
+    // dictionary read through L1/L2: RBPG leaves one slot's worth of the unified L1/shared array
+    // to the L1 cache that serves A (cfg3: 11 instead of 12 warps is +5%; FISTA measured -2%, so
+    // it keeps every slot; TB_WARPS_L1 overrides)
     const char* ev = getenv("TB_WARPS_L1");
-    const int cap_l1 = ev ? atoi(ev) : warps;
+    const int cap_l1 = ev ? atoi(ev) : (P.mode == SOLVER_RBPG && warps > 2 ? warps - 1 : warps);
     if (cap_l1 >= 1 && cap_l1 < warps) warps = cap_l1;
   }
   if (const char* wc = getenv("TB_WARPS_CAP")) {  // tuning/diagnostics: cap the warps per CTA
