@@ -84,10 +84,11 @@ int tb_set_partition(tb_ctx* ctx, int32_t num_blocks, const int64_t* starts_host
 /* L = 2 spectral_sq_norm(A) for ISTA/FISTA (solver.py:344). */
 int tb_set_lipschitz(tb_ctx* ctx, double lipschitz);
 
-/* default_lambda (prox.py:153-161): lambda_p = beta * max_k |(A^H b_p)_k|, stored float32.
+/* default_lambda (prox.py:153-161): lambda_p = beta * max_k |(A^H b_p)_k| as a double: the exact
+ * products of the complex64 inputs accumulated in fp64, as the reference's complex128 product.
  * pixels_dev: complex64 [P, n] (TSTK1 payload order, stack.py:46-52). */
 int tb_default_lambda(tb_ctx* ctx, const void* pixels_dev, int64_t num_pixels, double beta,
-                      float* lambda_dev, void* stream);
+                      double* lambda_dev, void* stream);
 
 /* Per-pixel seed rule of the CLI worker (cli.py:102):
  * seeds[i] = derive_seed(substream(run_seed, first_pixel_id + i)) (rng.py:17-29). */
@@ -95,7 +96,7 @@ int tb_derive_seeds(uint64_t run_seed, int64_t first_pixel_id, int64_t num_pixel
                     uint64_t* seeds_dev, void* stream);
 
 /* rbpg_solve / fista_solve / ista_solve (solver.py:250-390) over a pixel batch.
- *  pixels_dev  complex64 [P, n];  lambda_dev float32 [P];  seeds_dev uint64 [P] (RBPG only,
+ *  pixels_dev  complex64 [P, n];  lambda_dev double [P];  seeds_dev uint64 [P] (RBPG only,
  *  may be NULL otherwise);  x_dev complex64 [P, m] out (Solution.x_hat);
  *  f_final_dev double [P] out (objective_history[-1]);  history_dev double [P, hist_stride]
  *  out or NULL (objective_history, NaN-padded after iterations+1 entries);
@@ -103,7 +104,7 @@ int tb_derive_seeds(uint64_t run_seed, int64_t first_pixel_id, int64_t num_pixel
  *  Asynchronous on `stream`; not re-entrant per context (the context owns the solver workspace:
  *  the RBPG extrapolation memory of the on-chip solver and the tiled solver's state buffers). */
 int tb_solve(tb_ctx* ctx, int32_t solver, const tb_solver_config* cfg, const void* pixels_dev,
-             const float* lambda_dev, const uint64_t* seeds_dev, int64_t num_pixels, void* x_dev,
+             const double* lambda_dev, const uint64_t* seeds_dev, int64_t num_pixels, void* x_dev,
              double* f_final_dev, double* history_dev, int64_t hist_stride,
              int32_t* iterations_dev, int32_t* status_dev, void* stream);
 
@@ -117,7 +118,7 @@ int tb_solve(tb_ctx* ctx, int32_t solver, const tb_solver_config* cfg, const voi
  *  followed by [P][4] scalars), or NULL for an internal one.  State lives in HBM (3 fp64 copies
  *  of x per pixel). */
 int tb_tiled_create(tb_ctx* ctx, int32_t solver, const tb_solver_config* cfg, const void* pixels_dev,
-                    const float* lambda_dev, const uint64_t* seeds_dev, int64_t num_pixels,
+                    const double* lambda_dev, const uint64_t* seeds_dev, int64_t num_pixels,
                     double* history_dev, int64_t hist_stride, void* red_dev, void* stream,
                     tb_tiled** out);
 int tb_tiled_round_a(tb_tiled* h, void* stream);

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libtomobpdn_b200.so")
-SOURCES = ["tb_api.cu", "k_warp_solver.cu", "k_setup.cu", "k_select.cu", "k_tiled.cu", "k_rbpg_group.cu", "k_tc_adjoint.cu", "k_tc_tiled.cu"]
+SOURCES = ["tb_api.cu", "k_warp_solver.cu", "k_setup.cu", "k_select.cu", "k_tiled.cu", "k_tc_tiled.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

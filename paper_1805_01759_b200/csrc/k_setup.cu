@@ -12,43 +12,47 @@ namespace tb {
 // ------------------------------------------------------------------ default lambda
 // lambda_p = beta * max_k |(A^H b_p)_k| as a tiled complex GEMM with a max epilogue: a CTA owns 64
 // dictionary columns x 64 pixels; 16-row K slices of A and of the pixel chunk are staged in shared
-// memory and every thread accumulates a 4 x 4 (column x pixel) micro-tile (columns tc + 16 i, pixels
-// tp + 16 j: conflict-free / broadcast shared reads), so each A element fetched from HBM/L2 serves
-// 64 pixels instead of one.  The per-column sums run over the rows in order with the same fp32
-// fmaf sequence as a per-column loop; the column max is order-free, so it is merged across CTAs
-// with an integer atomicMax on the (non-negative) float bits and the result is deterministic.
+// memory (converted to fp64 once at staging) and every thread accumulates a 4 x 4 (column x pixel)
+// micro-tile (columns tc + 16 i, pixels tp + 16 j: conflict-free / broadcast shared reads), so each
+// A element fetched from HBM/L2 serves 64 pixels instead of one.  The products of the complex64
+// inputs are exact in fp64 and are accumulated in fp64, as the reference's complex128
+// `a.conj().T @ b` does (prox.py:159-161), so lambda is the reference's up to summation order
+// (~1e-16 relative) and is carried as a double end to end.  The column max is order-free, so it is
+// merged across CTAs with an integer atomicMax on the (non-negative) double bits: deterministic.
 constexpr int LT_C = 64, LT_P = 64, LT_K = 16;
 
 __global__ void __launch_bounds__(256) lambda_tile_kernel(const float2* __restrict__ A, int n, int m,
                                                           const float2* __restrict__ B, long long P,
-                                                          unsigned* __restrict__ bits) {
-  __shared__ float2 sa[LT_K][LT_C];
-  __shared__ float2 sb[LT_K][LT_P + 1];  // +1: conflict-light transposed staging stores
+                                                          unsigned long long* __restrict__ bits) {
+  __shared__ double2 sa[LT_K][LT_C];
+  __shared__ double2 sb[LT_K][LT_P + 1];  // +1: conflict-light transposed staging stores
   const int tid = threadIdx.x, tc = tid & 15, tp = tid >> 4;
   const long long c0 = (long long)blockIdx.x * LT_C;
   for (long long p0 = (long long)blockIdx.y * LT_P; p0 < P; p0 += (long long)gridDim.y * LT_P) {
-    float2 acc[4][4];
+    double2 acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+      for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
     for (int k0 = 0; k0 < n; k0 += LT_K) {
       for (int e = tid; e < LT_K * LT_C; e += 256) {
         const int kk = e / LT_C, cc = e % LT_C;
         const long long c = c0 + cc;
         const int i = k0 + kk;
-        sa[kk][cc] = (i < n && c < m) ? __ldg(&A[(size_t)i * m + c]) : make_float2(0.f, 0.f);
+        const float2 v = (i < n && c < m) ? __ldg(&A[(size_t)i * m + c]) : make_float2(0.f, 0.f);
+        sa[kk][cc] = make_double2(v.x, v.y);
       }
       for (int e = tid; e < LT_K * LT_P; e += 256) {
         const int pp = e / LT_K, kk = e % LT_K;
         const long long p = p0 + pp;
         const int i = k0 + kk;
-        sb[kk][pp] = (i < n && p < P) ? __ldg(&B[(size_t)p * n + i]) : make_float2(0.f, 0.f);
+        const float2 v = (i < n && p < P) ? __ldg(&B[(size_t)p * n + i]) : make_float2(0.f, 0.f);
+        sb[kk][pp] = make_double2(v.x, v.y);
       }
       __syncthreads();
       const int kn = min(LT_K, n - k0);
       for (int kk = 0; kk < kn; ++kk) {
-        float2 a[4], b[4];
+        double2 a[4], b[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = sa[kk][tc + 16 * i];
 #pragma unroll
@@ -56,33 +60,37 @@ __global__ void __launch_bounds__(256) lambda_tile_kernel(const float2* __restri
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) cfma_conj(acc[i][j], a[i], b[j]);
+          for (int j = 0; j < 4; ++j) {
+            // conj(a) b
+            acc[i][j].x = fma(a[i].x, b[j].x, fma(a[i].y, b[j].y, acc[i][j].x));
+            acc[i][j].y = fma(a[i].x, b[j].y, fma(-a[i].y, b[j].x, acc[i][j].y));
+          }
       }
       __syncthreads();
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      float best = 0.f;
+      double best = 0.0;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (c0 + tc + 16 * i < m) best = fmaxf(best, cabsf(acc[i][j]));
+        if (c0 + tc + 16 * i < m) best = fmax(best, hypot(acc[i][j].x, acc[i][j].y));
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(TB_FULL_MASK, best, o));
+      for (int o = 8; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(TB_FULL_MASK, best, o));
       const long long p = p0 + tp + 16 * j;
-      if (tc == 0 && p < P) atomicMax(&bits[p], __float_as_uint(best));
+      if (tc == 0 && p < P) atomicMax(&bits[p], (unsigned long long)__double_as_longlong(best));
     }
   }
 }
 
-__global__ void lambda_finish_kernel(float* lam, long long P, double beta) {
+__global__ void lambda_finish_kernel(double* lam, long long P, double beta) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < P) lam[p] = (float)(beta * (double)lam[p]);
+  if (p < P) lam[p] = beta * lam[p];
 }
 
 cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B, long long P, double beta,
-                                  float* lam, int num_sms, cudaStream_t st) {
+                                  double* lam, int num_sms, cudaStream_t st) {
   if (P <= 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(lam, 0, sizeof(float) * (size_t)P, st);  // +0.0f bits: the max identity
+  cudaError_t e = cudaMemsetAsync(lam, 0, sizeof(double) * (size_t)P, st);  // +0.0 bits: the max identity
   if (e != cudaSuccess) return e;
   const long long ctiles = (m + LT_C - 1) / LT_C, pchunks = (P + LT_P - 1) / LT_P;
   long long gy = (long long)num_sms * 8 / ctiles;
@@ -91,7 +99,7 @@ cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B
   if (gy > 65535) gy = 65535;
   if (ctiles > 0x7fffffffll) return cudaErrorInvalidValue;
   count_launch();
-  lambda_tile_kernel<<<dim3((unsigned)ctiles, (unsigned)gy), 256, 0, st>>>(A, n, m, B, P, reinterpret_cast<unsigned*>(lam));
+  lambda_tile_kernel<<<dim3((unsigned)ctiles, (unsigned)gy), 256, 0, st>>>(A, n, m, B, P, reinterpret_cast<unsigned long long*>(lam));
   count_launch();
   lambda_finish_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(lam, P, beta);
   return cudaGetLastError();

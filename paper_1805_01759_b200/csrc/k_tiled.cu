@@ -630,8 +630,14 @@ cudaError_t tiled_prep(const TiledParams& T, cudaStream_t st) {
   tiled_prep_kernel<<<warp_grid(T.P), 256, 0, st>>>(T);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  // bucket counters: 3 ints per block in dynamic shared memory (tb_tiled_create bounds J)
+  const size_t sched_smem = 3 * (size_t)T.J * sizeof(int);
+  if (sched_smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(tiled_schedule_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sched_smem);
+    if (e != cudaSuccess) return e;
+  }
   count_launch();
-  tiled_schedule_kernel<<<1, 1024, 3 * T.J * sizeof(int), st>>>(T);
+  tiled_schedule_kernel<<<1, 1024, sched_smem, st>>>(T);
   return cudaGetLastError();
 }
 

@@ -131,8 +131,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
   double2* xs = DC ? rv + n : apv + n;           // x (fp64 iterate)
   double2* zs = xs + m;                          // broadcast buffer for forward products [max_width]
   float4* ryv = reinterpret_cast<float4*>(zs + P.max_width);  // r_y rounded, as (r.x, r.y, r.y, -r.x)
-  float2* ds = reinterpret_cast<float2*>(ryv + n);  // d = x - prev, fp32 (y = x + m_k d); not DC
-  float2* bv = ds + m;                           // b; not RBPG
+  double2* ds = reinterpret_cast<double2*>(ryv + n);  // d = x - prev, fp64 (y = x + m_k d); not DC
+  float2* bv = reinterpret_cast<float2*>(ds + m);  // b; not RBPG
   double2* dlt = reinterpret_cast<double2*>(ryv + n);  // DC: delta [J][n]
   double* ring = DC ? reinterpret_cast<double*>(dlt + (size_t)J * n) : reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
   double* l1blk = ring + 16;                     // RBPG: sum |x_b| per block (updated on accept)
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       if (DC)
         dg[c] = make_double2(0.0, 0.0);
       else
-        ds[c] = make_float2(0.f, 0.f);
+        ds[c] = make_double2(0.0, 0.0);
     }
     if (DC)
       for (int e = lane; e < J * n; e += 32) dlt[e] = make_double2(0.0, 0.0);
@@ -311,11 +311,11 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         const double2 xv = xs[col];
         double2 yv = xv;
         if (!ista) {
-          // y = x + m_k (x - prev) with the extrapolation memory kept as d = x - prev in fp32;
+          // y = x + m_k (x - prev) with the extrapolation memory kept as d = x - prev in fp64;
           // d is exactly 0 after a rejected visit, so `np.any(dy)` (solver.py:291) is preserved
-          const float2 dv = ds[col];
-          yv.x = fma(mk, (double)dv.x, xv.x);
-          yv.y = fma(mk, (double)dv.y, xv.y);
+          const double2 dv = ds[col];
+          yv.x = fma(mk, dv.x, xv.x);
+          yv.y = fma(mk, dv.y, xv.y);
         }
         bool nz = false;
         double2 dyv = make_double2(0.0, 0.0);
@@ -421,9 +421,9 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
             yv.x = fma(mk, dvb[t].x, xv.x);
             yv.y = fma(mk, dvb[t].y, xv.y);
           } else if (!ista) {
-            const float2 dv = ds[col];
-            yv.x = fma(mk, (double)dv.x, xv.x);
-            yv.y = fma(mk, (double)dv.y, xv.y);
+            const double2 dv = ds[col];
+            yv.x = fma(mk, dv.x, xv.x);
+            yv.y = fma(mk, dv.y, xv.y);
           }
           const double2 v = make_double2(fma(-alpha, (double)g[t].x, yv.x), fma(-alpha, (double)g[t].y, yv.y));
           const double mag2 = fma(v.x, v.x, v.y * v.y);
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
             if (DC)
               dg[cs + cl] = make_double2(zv.x - xv.x, zv.y - xv.y);
             else
-              ds[cs + cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
+              ds[cs + cl] = make_double2(zv.x - xv.x, zv.y - xv.y);
             xs[cs + cl] = zv;
           }
         }
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           if (cl < width) {
             const double2 xv = xs[cl];
             const double2 zv = (masks[t] >> lane) & 1u ? zs[base + __popc(masks[t] & lt_mask)] : make_double2(0.0, 0.0);
-            ds[cl] = make_float2((float)(zv.x - xv.x), (float)(zv.y - xv.y));
+            ds[cl] = make_double2(zv.x - xv.x, zv.y - xv.y);
             xs[cl] = zv;
           }
           base += __popc(masks[t]);

@@ -8,7 +8,7 @@
 namespace tb {
 
 cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B, long long P, double beta,
-                                  float* lam, int num_sms, cudaStream_t st);
+                                  double* lam, int num_sms, cudaStream_t st);
 cudaError_t launch_derive_seeds(uint64_t run_seed, long long first, long long P, uint64_t* seeds, cudaStream_t st);
 cudaError_t launch_power_small(const float2* A, int n, int m, const long long* starts, const long long* stops,
                                int num_ranges, double2* v, double2* uscratch, int max_iter, double rtol,

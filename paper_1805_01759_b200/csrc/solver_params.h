@@ -25,7 +25,7 @@ struct SolveParams {
   int total_iters, fixed, cap;
   double tol, c_alpha, alpha_scale;
   const float2* B;
-  const float* lam;
+  const double* lam;
   const uint64_t* seeds;
   long long num_pixels;
   float2* X;
@@ -44,11 +44,11 @@ struct SolveParams {
 #define TB_WS_DCACHE 1
 #endif
 
-// per-warp shared bytes: 2 fp64 n-vectors, fp64 x (m) + fp64 broadcast buffer (width), fp32 d = x - prev
-// (m), fp32 r_y as float4 + fp32 b (n each), 16-double ring, J-double per-block l1 cache, 32 buffered
-// Philox outputs, width ints (compacted nonzero columns)
+// per-warp shared bytes (ISTA/FISTA): 2 fp64 n-vectors, fp64 x (m) + fp64 broadcast buffer (width),
+// fp64 d = x - prev (m), fp32 r_y as float4 + fp32 b (n each), 16-double ring, J-double per-block l1
+// cache, 32 buffered Philox outputs, width ints (compacted nonzero columns)
 __host__ __device__ inline size_t warp_slot_bytes(int n, int m, int width, int J) {
-  size_t b = (size_t)n * 32 + (size_t)(m + width) * 16 + (size_t)m * 8 + (size_t)n * 24 + 16 * 8 + (size_t)J * 8 + 32 * 8 + (size_t)width * 4;
+  size_t b = (size_t)n * 32 + (size_t)(m + width) * 16 + (size_t)m * 16 + (size_t)n * 24 + 16 * 8 + (size_t)J * 8 + 32 * 8 + (size_t)width * 4;
   return (b + 15) & ~(size_t)15;
 }
 // RBPG slot with the delta cache: fp64 r, fp64 x (m), fp64 broadcast buffer (width), r_y quads (n),
@@ -66,15 +66,6 @@ __host__ __device__ inline size_t block_table_bytes(int J) {
   return (b + 15) & ~(size_t)15;
 }
 
-// RBPG group-kernel slot: fp64 r, fp64 x, fp64 broadcast [width], fp32 d = x - prev, fp32 r_y,
-// 16-double ring, J-double per-block l1 cache
-__host__ __device__ inline size_t rbpg_slot_bytes(int n, int m, int width, int J) {
-  size_t b = (size_t)n * 16 + (size_t)m * 16 + (size_t)width * 16 + (size_t)m * 8 + (size_t)(n + (n & 1)) * 8 + 16 * 8 + (size_t)J * 8;
-  return (b + 15) & ~(size_t)15;
-}
-
 cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps);
-bool rbpg_group_supported(int n, int max_width);
-cudaError_t launch_rbpg_group(const SolveParams& P, int num_sms, cudaStream_t st);
 
 }  // namespace tb

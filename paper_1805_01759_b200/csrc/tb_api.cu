@@ -40,7 +40,25 @@ struct tb_ctx {
   // warp solver RBPG extrapolation memory (fp64 d per warp slot), grow-only
   double2* dglob = nullptr;
   size_t dglob_elems = 0;
+  // Ordering of the context's mutable device state (queue counter, dglob, mk, ws) across streams:
+  // every launch that uses it records `done` on its stream, and a launch on another stream first
+  // waits on `done`, so solves issued on different streams serialise instead of racing; buffers
+  // are only freed / reallocated after `done` has completed.
+  cudaEvent_t done = nullptr;
+  cudaStream_t last = nullptr;
 };
+
+// Order `st` after the previous user of the context's mutable state (see tb_ctx::done).
+static cudaError_t ctx_acquire(tb_ctx* c, cudaStream_t st) {
+  if (c->done && c->last != st) return cudaStreamWaitEvent(st, c->done, 0);
+  return cudaSuccess;
+}
+static cudaError_t ctx_release(tb_ctx* c, cudaStream_t st) {
+  c->last = st;
+  return cudaEventRecord(c->done, st);
+}
+// Wait until no launch uses the context's mutable state (before freeing or reallocating it).
+static cudaError_t ctx_drain(tb_ctx* c) { return c->done ? cudaEventSynchronize(c->done) : cudaSuccess; }
 
 struct tb_tiled {
   tb_ctx* ctx = nullptr;
@@ -128,6 +146,7 @@ int tb_ctx_create(int device, const void* dictionary_dev, int64_t n, int64_t m, 
   cudaError_t e = cudaMalloc(&c->A, sizeof(float2) * n * m);
   if (e == cudaSuccess) e = cudaMemcpy(c->A, dictionary_dev, sizeof(float2) * n * m, cudaMemcpyDeviceToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&c->queue, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     cudaFree(c->A);
     delete c;
@@ -140,6 +159,8 @@ int tb_ctx_create(int device, const void* dictionary_dev, int64_t n, int64_t m, 
 int tb_ctx_destroy(tb_ctx* c) {
   if (!c) return TB_OK;
   cudaSetDevice(c->device);
+  ctx_drain(c);
+  if (c->done) cudaEventDestroy(c->done);
   cudaFree(c->A);
   cudaFree(c->blk_start);
   cudaFree(c->blk_lip);
@@ -280,7 +301,7 @@ int tb_set_lipschitz(tb_ctx* c, double lip) {
   return TB_OK;
 }
 
-int tb_default_lambda(tb_ctx* c, const void* pixels, int64_t P, double beta, float* lam, void* stream) {
+int tb_default_lambda(tb_ctx* c, const void* pixels, int64_t P, double beta, double* lam, void* stream) {
   if (!c || (P > 0 && (!pixels || !lam))) return fail(TB_ERR_INVALID, "null argument");
   if (P < 0) return fail(TB_ERR_INVALID, "num_pixels must be >= 0");
   TB_CUDA(cudaSetDevice(c->device));
@@ -318,10 +339,13 @@ static int check_solve_args(tb_ctx* c, int32_t solver, const tb_solver_config* c
 
 static int ensure_mk(tb_ctx* c, int total, cudaStream_t st) {
   if (c->mk_len >= total + 1) return TB_OK;
+  // a live tiled handle points at the current table
+  if (c->ws_busy) return fail(TB_ERR_INVALID, "context busy: a tiled solve with fewer iterations is in flight");
   // theta_k = 2/(k+1) collapsed to m_k = (k-2)/(k+1) (solver.py:222-224), IEEE double division
   std::vector<double> h(total + 1);
   for (int k = 0; k <= total; ++k) h[k] = (k - 2.0) / (k + 1.0);
   TB_CUDA(cudaStreamSynchronize(st));
+  TB_CUDA(ctx_drain(c));
   cudaFree(c->mk);
   c->mk = nullptr;
   TB_CUDA(cudaMalloc(&c->mk, sizeof(double) * (total + 1)));
@@ -341,7 +365,7 @@ static bool warp_path_fits(tb_ctx* c, int32_t solver) {
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const float* lam,
+int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const double* lam,
                     const uint64_t* seeds, int64_t P, double* hist, int64_t hist_stride, void* red_dev,
                     void* stream, tb_tiled** out) {
   int rc = check_solve_args(c, solver, cfg, seeds, P, hist, hist_stride);
@@ -354,6 +378,8 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   if (rc != TB_OK) return rc;
   const bool rb = solver == TB_SOLVER_RBPG;
   const int J = rb ? c->num_blocks : 1;
+  if (3ll * J * (long long)sizeof(int) > 227ll * 1024)
+    return fail(TB_ERR_INVALID, "num_blocks %d exceeds the tiled scheduler's %d-block limit", J, (int)(227 * 1024 / (3 * sizeof(int))));
   const int n = (int)c->n;
   const long long m = c->m;
   const int maxw = rb ? c->max_block_width : (int)m;
@@ -424,6 +450,7 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   if (c->ws_busy) return fail(TB_ERR_INVALID, "one tiled solve per context at a time");
   if (c->ws_size < tot) {
     TB_CUDA(cudaStreamSynchronize(st));
+    TB_CUDA(ctx_drain(c));
     cudaFree(c->ws);
     c->ws = nullptr;
     c->ws_size = 0;
@@ -433,6 +460,7 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
     TB_CUDA(cudaMalloc((void**)&c->ws, tot));
     c->ws_size = tot;
   }
+  TB_CUDA(ctx_acquire(c, st));
   unsigned char* base = c->ws;
   tb_tiled* h = new tb_tiled();
   h->ctx = c;
@@ -544,6 +572,7 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   const int rem = (int)P;
   TB_CUDA(cudaMemcpyAsync(T.remaining, &rem, sizeof(int), cudaMemcpyHostToDevice, st));
   TB_CUDA(tb::tiled_init(T, st));
+  TB_CUDA(ctx_release(c, st));
   TB_CUDA(cudaStreamSynchronize(st));
   c->ws_busy = true;
   *out = h;
@@ -554,19 +583,23 @@ int tb_tiled_round_a(tb_tiled* h, void* stream) {
   if (!h) return fail(TB_ERR_INVALID, "null handle");
   cudaStream_t st = (cudaStream_t)stream;
   TB_CUDA(cudaSetDevice(h->ctx->device));
+  TB_CUDA(ctx_acquire(h->ctx, st));
   TB_CUDA(tb::tiled_prep(h->T, st));
   if (h->G)
     TB_CUDA(tb::tc_adjoint_round(h->T, h->Apk, h->Rpk, h->tile_base, h->nck, h->tc_max_tiles, h->tc_tiles_per_split,
                                  h->tc_splits, h->G, st));
   TB_CUDA(tb::tiled_pass(h->T, h->ctx->num_sms, st));
   TB_CUDA(tb::tiled_reduce(h->T, st));
+  TB_CUDA(ctx_release(h->ctx, st));
   return TB_OK;
 }
 
 int tb_tiled_round_b(tb_tiled* h, void* stream) {
   if (!h) return fail(TB_ERR_INVALID, "null handle");
   TB_CUDA(cudaSetDevice(h->ctx->device));
+  TB_CUDA(ctx_acquire(h->ctx, (cudaStream_t)stream));
   TB_CUDA(tb::tiled_update(h->T, (cudaStream_t)stream));
+  TB_CUDA(ctx_release(h->ctx, (cudaStream_t)stream));
   h->rounds++;
   return TB_OK;
 }
@@ -574,6 +607,7 @@ int tb_tiled_round_b(tb_tiled* h, void* stream) {
 int tb_tiled_remaining(tb_tiled* h, int64_t* out, void* stream) {
   if (!h || !out) return fail(TB_ERR_INVALID, "null argument");
   int v = 0;
+  TB_CUDA(ctx_acquire(h->ctx, (cudaStream_t)stream));
   TB_CUDA(cudaMemcpyAsync(&v, h->T.remaining, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   TB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   *out = v;
@@ -587,8 +621,10 @@ int tb_tiled_finish(tb_tiled* h, void* x, double* f_final, int32_t* iters, int32
   h->T.X = (float2*)x;
   h->T.f_final = f_final;
   h->T.iters = iters;
+  TB_CUDA(ctx_acquire(h->ctx, st));
   TB_CUDA(tb::tiled_finish(h->T, st));
   TB_CUDA(cudaMemcpyAsync(status, h->T.status, sizeof(int) * h->T.P, cudaMemcpyDeviceToDevice, st));
+  TB_CUDA(ctx_release(h->ctx, st));
   return TB_OK;
 }
 
@@ -601,7 +637,7 @@ int tb_tiled_destroy(tb_tiled* h) {
   return TB_OK;
 }
 
-static int solve_tiled(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const float* lam,
+static int solve_tiled(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const double* lam,
                        const uint64_t* seeds, int64_t P, void* x, double* f_final, double* hist, int64_t hist_stride,
                        int32_t* iters, int32_t* status, cudaStream_t st) {
   // pixel chunks sized to the free HBM (state is 3 fp64 copies of x per pixel)
@@ -641,7 +677,7 @@ static int solve_tiled(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, c
   return TB_OK;
 }
 
-int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const float* lam,
+int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const double* lam,
              const uint64_t* seeds, int64_t P, void* x, double* f_final, double* hist, int64_t hist_stride,
              int32_t* iters, int32_t* status, void* stream) {
   int rc = check_solve_args(c, solver, cfg, seeds, P, hist, hist_stride);
@@ -689,6 +725,7 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
     const size_t need = (size_t)c->num_sms * 32 * (size_t)c->m;  // >= resident warp slots x m
     if (c->dglob_elems < need) {
       TB_CUDA(cudaStreamSynchronize(st));
+      TB_CUDA(ctx_drain(c));
       cudaFree(c->dglob);
       c->dglob = nullptr;
       c->dglob_elems = 0;
@@ -697,16 +734,11 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
     }
     S.dglob = c->dglob;
   }
+  TB_CUDA(ctx_acquire(c, st));
   TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
-  const char* force = getenv("TB_RBPG_KERNEL");
-  // the half-warp-per-pixel RBPG variant measured slower on cfg2 (0.68 vs 1.07 M px/s); opt-in only
-  const bool use_group = solver == TB_SOLVER_RBPG && tb::rbpg_group_supported(S.n, S.max_width) && force && strcmp(force, "group") == 0;
-  if (use_group) {
-    TB_CUDA(tb::launch_rbpg_group(S, c->num_sms, st));
-  } else {
-    int warps = 0;
-    TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
-  }
+  int warps = 0;
+  TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
+  TB_CUDA(ctx_release(c, st));
   return TB_OK;
 }
 

@@ -32,7 +32,7 @@ struct TiledParams {
   // batch (chunk)
   int P;
   const float2* B;       // [P][n]
-  const float* lam;      // [P]
+  const double* lam;     // [P]
   const uint64_t* seeds; // [P]
   double2* X3;           // 3 x [P][m] fp64 state buffers
   // Tile occupancy of the state buffers: occ[buf][p][t] == 0 means TL_CT-column tile t of buffer

@@ -109,7 +109,7 @@ def solve_column_sharded(shards, pixels, lam, config: SolverConfig, seeds=None, 
         d = sh.d
         dev = d.device
         b = d._pixels(pixels)
-        lam_t = torch.as_tensor(lam, dtype=torch.float32).reshape(-1).to(dev)
+        lam_t = torch.as_tensor(lam, dtype=torch.float64).reshape(-1).to(dev)
         seeds_t = None
         if backend == "rbpg":
             seeds_t = seeds.to(dev).view(torch.uint64) if isinstance(seeds, torch.Tensor) else torch.from_numpy(np.asarray(seeds, dtype=np.uint64)).to(dev)

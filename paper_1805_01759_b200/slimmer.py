@@ -164,7 +164,7 @@ def pipeline_batch(dictionary, pixels, grid: ParameterGrid, config: PipelineConf
     if lam is None:
         lam_t = d.default_lambda(b, beta) if config.solver.lambda_reg is None else None
         if lam_t is None:
-            lam_t = np.full(p, float(config.solver.lambda_reg), dtype=np.float32)
+            lam_t = np.full(p, float(config.solver.lambda_reg), dtype=np.float64)
     else:
         lam_t = lam
     if config.backend == "rbpg" and seeds is None:

@@ -319,10 +319,10 @@ class Dictionary:
         return t.contiguous()
 
     def default_lambda(self, pixels, beta: float = 0.05):
-        """beta * max |A^H b| per pixel, float32 device tensor (prox.py:153-161)."""
+        """beta * max |A^H b| per pixel, float64 device tensor (prox.py:153-161)."""
         torch = _torch()
         b = self._pixels(pixels)
-        lam = torch.empty(b.shape[0], dtype=torch.float32, device=self.device)
+        lam = torch.empty(b.shape[0], dtype=torch.float64, device=self.device)
         with torch.cuda.device(self.device):
             _lib.check(self._lib.tb_default_lambda(self._h, _lib.ptr(b), b.shape[0], float(beta), _lib.ptr(lam), self._stream()))
         return lam
@@ -352,7 +352,7 @@ class Dictionary:
             lam_h = np.asarray(lam, dtype=np.float64).reshape(-1)
             if not (np.all(np.isfinite(lam_h)) and np.all(lam_h >= 0)):
                 raise ConfigurationError("lambda_reg must be finite and >= 0")  # prox.py:47-48
-        lam_t = torch.as_tensor(lam, dtype=torch.float32).reshape(-1).to(self.device)
+        lam_t = torch.as_tensor(lam, dtype=torch.float64).reshape(-1).to(self.device)
         if lam_t.numel() == 1 and p != 1:
             lam_t = lam_t.expand(p).contiguous()
         if lam_t.numel() != p:

@@ -82,13 +82,14 @@ def test_golden_cfg1_solvers(tb, golden, cfg1, backend):
     ff = bs.objective_final.cpu().numpy()
     rit, rst, rx = golden[f"cfg1/{backend}/iters"], golden[f"cfg1/{backend}/status"], golden[f"cfg1/{backend}/x"]
     rf = np.array([golden[f"cfg1/{backend}/hist"][p][rit[p]] for p in range(len(rit))])
+    # every solver (FISTA included: its extrapolation memory is fp64, so y and A y agree) stops at
+    # the reference's iteration with the reference's status on every golden pixel
     assert np.array_equal(st, rst)
-    if backend != "fista":
-        assert np.array_equal(it, rit)
+    assert np.array_equal(it, rit)
     np.testing.assert_allclose(ff, rf, rtol=1e-4)
     err = np.linalg.norm(x - rx, axis=1) / np.maximum(np.linalg.norm(rx, axis=1), 1e-30)
     assert np.median(err) <= 1e-4
-    assert err.max() <= (5e-2 if backend == "fista" else 1e-3)
+    assert err.max() <= 1e-3
     # early history (before trajectories can drift) tracks the reference closely
     h = bs.history.cpu().numpy()
     k = 30
