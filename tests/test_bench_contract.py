@@ -1,10 +1,13 @@
-"""bench.py contract on CPU: the reference arm (the oracle port on host cores) prints ONE JSON
-line with the driver's keys.  The GPU arm's line is exercised by the driver on a B200."""
+"""bench.py contract on CPU: the reference arm (the unmodified reference on host cores, or the
+oracle port when it is not installed) prints ONE JSON line with the driver's keys.  The GPU arm's
+line is exercised by the driver on a B200."""
 
 import json
 import os
 import subprocess
 import sys
+
+sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 
@@ -23,7 +26,9 @@ def test_reference_arm_json_line():
         assert key in d, key
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["config"]["workload"] == "cfg2"
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] == d["value"]
+    from oracle import reference_arm as R
+
+    assert d["cpu_baseline"]["kind"] == ("reference" if R.locate() else "port") and d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
