@@ -1,0 +1,169 @@
+"""BASELINE cfg4 and cfg5 at the BASELINE settings against the REAL reference (golden_large_v1.npz,
+made by tests/golden/make_golden_large.py in the build container).
+
+cfg4 (n=100, m=160,000): 8 pixels sampled across the 16,384-pixel batch, FISTA and RBPG with
+max_iters=500 / tol=1e-6, then selection with k_max=2 (solver.py:250-376, slimmer.py:77-212).
+cfg5 (n=100, m=1,048,576): 2 right-hand sides, FISTA and RBPG with fixed_iters=60 and RBPG to its
+stop rule, selection with k_max=3 -- unsharded and column-sharded (the multi-GPU algorithm,
+emulated with 2 and 4 shards on one device).
+
+The dictionaries are rebuilt from the package's seeded synthesis and proven identical to the
+ones the reference consumed by their SHA-256.  Identical inputs (b, lambda, seeds) on both sides.
+
+Tolerances: status and support exact; iteration counts exact; final objective 1e-6 relative
+(observed ~1e-9), the whole objective history 1e-5 relative; x_hat relative L2 error 1e-4;
+debiased amplitudes 1e-6 relative (same support => the same fp64 least squares); BIC scores 1e-8.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+STATUS_NAMES = ["converged", "max-iters", "line-search-failure", "numerical-failure"]
+
+
+@pytest.fixture(scope="module")
+def tb():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_1805_01759_b200 as tb
+
+    return tb
+
+
+@pytest.fixture(scope="module")
+def big():
+    return np.load(os.path.join(ROOT, "tests", "golden", "golden_large_v1.npz"))
+
+
+def _batch(big, cfg):
+    from paper_1805_01759_b200.synth import make_config
+
+    ids = big[f"cfg{cfg}/ids"]
+    batch = make_config(cfg, num_pixels=int(ids.max()) + 1)
+    sha = hashlib.sha256(np.ascontiguousarray(batch.dictionary).tobytes()).hexdigest()
+    assert sha == str(big[f"cfg{cfg}/a_sha256"]), "rebuilt dictionary differs from the one the reference solved with"
+    np.testing.assert_array_equal(batch.pixels[ids], big[f"cfg{cfg}/b"])
+    return batch
+
+
+@pytest.fixture(scope="module")
+def cfg4(tb, big):
+    batch = _batch(big, 4)
+    return batch, tb.Dictionary(batch.dictionary)
+
+
+@pytest.fixture(scope="module")
+def cfg5(tb, big):
+    batch = _batch(big, 5)
+    return batch, tb.Dictionary(batch.dictionary)
+
+
+def _ref_x(big, key, m):
+    x = np.zeros(m, dtype=np.complex128)
+    x[big[f"{key}/x_idx"]] = big[f"{key}/x_val"]
+    return x
+
+
+def _check_solution(big, tag, sol, m, p_count, hist_rtol=1e-5):
+    its = sol.iterations.cpu().numpy()
+    st = sol.status.cpu().numpy()
+    ff = sol.objective_final.cpu().numpy()
+    hist = sol.history.cpu().numpy()
+    for j in range(p_count):
+        key = f"{tag}/{j}"
+        assert int(st[j]) == int(big[f"{key}/status"]), (key, STATUS_NAMES[st[j]])
+        assert int(its[j]) == int(big[f"{key}/iters"]), key
+        rh = big[f"{key}/hist"]
+        assert ff[j] == pytest.approx(rh[-1], rel=1e-6), key
+        np.testing.assert_allclose(hist[j, : rh.size], rh, rtol=hist_rtol, err_msg=key)
+        rx = _ref_x(big, key, m)
+        gx = sol.x_hat[j].cpu().numpy().astype(np.complex128)
+        err = np.linalg.norm(gx - rx) / max(np.linalg.norm(rx), 1e-30)
+        assert err <= 1e-4, (key, err)
+
+
+def _check_selection(big, tag, est, p_count):
+    order = est.model_order.cpu().numpy()
+    sup = est.support.cpu().numpy()
+    amps = est.amplitudes.cpu().numpy()
+    sc = est.selection_scores.cpu().numpy()
+    el = est.elevations.cpu().numpy()
+    mo = est.motion_params.cpu().numpy()
+    for j in range(p_count):
+        key = f"{tag}/{j}"
+        k = int(big[f"{key}/order"])
+        assert int(order[j]) == k, key
+        assert list(sup[j, :k]) == list(big[f"{key}/support"]), key
+        np.testing.assert_allclose(amps[j, :k], big[f"{key}/amps"], rtol=1e-6, atol=1e-12, err_msg=key)
+        np.testing.assert_allclose(el[j, :k], big[f"{key}/elevs"], err_msg=key)
+        np.testing.assert_allclose(mo[j, :k], big[f"{key}/motion"], err_msg=key)
+        rs = big[f"{key}/scores"]
+        np.testing.assert_allclose(sc[j, : rs.size], rs, rtol=1e-8, atol=1e-8, err_msg=key)
+
+
+def test_cfg4_lambda_and_seeds(tb, big, cfg4):
+    """The device lambda rule and seed rule on the sampled pixels (prox.py:153-161, cli.py:102)."""
+    batch, d = cfg4
+    ids = big["cfg4/ids"]
+    lam = d.default_lambda(big["cfg4/b"], 0.1).cpu().numpy()
+    np.testing.assert_allclose(lam, big["cfg4/lam"].astype(np.float64), rtol=1e-7)  # fixture lambda is float32-rounded
+    seeds = np.array([int(d.derive_seeds(2018, 1, int(i)).cpu().numpy()[0]) for i in ids], dtype=np.uint64)
+    np.testing.assert_array_equal(seeds, [big[f"cfg4/rbpg_conv/{j}/seed"] for j in range(len(ids))])
+
+
+@pytest.mark.parametrize("backend", ["fista", "rbpg"])
+def test_cfg4_baseline_settings_vs_reference(tb, big, cfg4, backend):
+    batch, d = cfg4
+    n_px = len(big["cfg4/ids"])
+    tag = f"cfg4/{backend}_conv"
+    seeds = np.array([big[f"{tag}/{j}/seed"] for j in range(n_px)], dtype=np.uint64) if backend == "rbpg" else None
+    cfg = tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8)
+    sol = d.solve(big["cfg4/b"], big["cfg4/lam"].astype(np.float64), cfg, backend, seeds=seeds, history=True)
+    _check_solution(big, tag, sol, batch.m, n_px)
+    est = tb.select_batch(d, sol.x_hat, big["cfg4/b"], batch.grid, 2)
+    _check_selection(big, tag, est, n_px)
+
+
+@pytest.mark.parametrize("backend,mode", [("fista", "fixed60"), ("rbpg", "fixed60"), ("rbpg", "conv")])
+def test_cfg5_baseline_settings_vs_reference(tb, big, cfg5, backend, mode):
+    batch, d = cfg5
+    tag = f"cfg5/{backend}_{mode}"
+    seeds = np.array([big[f"{tag}/{j}/seed"] for j in range(2)], dtype=np.uint64) if backend == "rbpg" else None
+    cfg = tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8) if mode == "conv" else tb.SolverConfig(fixed_iters=60, tol=1e-6, num_blocks=8)
+    sol = d.solve(big["cfg5/b"], big["cfg5/lam"].astype(np.float64), cfg, backend, seeds=seeds, history=True)
+    _check_solution(big, tag, sol, batch.m, 2)
+    if mode == "conv":
+        est = tb.select_batch(d, sol.x_hat, big["cfg5/b"], batch.grid, 3)
+        _check_selection(big, tag, est, 2)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_cfg5_column_sharded_vs_reference(tb, big, cfg5, world):
+    """The cfg5 multi-GPU algorithm (columns sharded, striped RBPG blocks, one reduction per
+    round) at the BASELINE settings, `world` shards emulated on one device, against the reference."""
+    from paper_1805_01759_b200.sharded import ColumnShard, column_shards, gather_columns, local_columns, solve_column_sharded
+
+    batch, d = cfg5
+    tag = "cfg5/rbpg_conv"
+    seeds = np.array([big[f"{tag}/{j}/seed"] for j in range(2)], dtype=np.uint64)
+    lips = d.partition(8).lipschitz
+    ranges = column_shards(batch.m, world, 8)
+    shards = [ColumnShard(batch.dictionary[:, local_columns(r)], r, "rbpg", 8, lips) for r in ranges]
+    cfg = tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8)
+    outs = solve_column_sharded(shards, big["cfg5/b"], big["cfg5/lam"].astype(np.float64), cfg, seeds=seeds, history=True)
+    x = gather_columns([o.x_hat.cpu().numpy() for o in outs], ranges, batch.m)
+    for j in range(2):
+        key = f"{tag}/{j}"
+        for o in outs:
+            assert int(o.iterations[j]) == int(big[f"{key}/iters"])
+            assert int(o.status[j]) == int(big[f"{key}/status"])
+            assert float(o.objective_final[j]) == pytest.approx(big[f"{key}/hist"][-1], rel=1e-6)
+        rx = _ref_x(big, key, batch.m)
+        assert np.linalg.norm(x[j] - rx) / np.linalg.norm(rx) <= 1e-4

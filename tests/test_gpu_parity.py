@@ -318,3 +318,27 @@ def test_full_size_sampled_vs_oracle(tb, cfg_id, backend):
     sup, order = est.support.cpu().numpy()[idx], est.model_order.cpu().numpy()[idx]
     for k in range(len(idx)):
         assert list(sup[k, : order[k]]) == list(ref[k]["support"]), (int(idx[k]), sup[k], ref[k]["support"])
+
+
+@pytest.mark.parametrize("backend", ["rbpg", "fista"])
+def test_oracle_own_lambda_cfg1(tb, backend):
+    """No shared lambda: the GPU computes its own fp64 lambda rule, the oracle its own
+    (prox.py:153-161 in fp64 on the same complex64 inputs); solves and selection still agree."""
+    batch = _cfg_batch(tb, 1, 128)
+    d = tb.Dictionary(batch.dictionary)
+    a = batch.dictionary.astype(np.complex128)
+    pc = tb.PipelineConfig(solver=tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8, seed=2018), backend=backend, k_max=2)
+    est = tb.pipeline_batch(d, batch.pixels, batch.grid, pc, beta=0.1)
+    lam_gpu = est.lam.cpu().numpy()
+    lam_ref = np.array([O.default_lambda(a, batch.pixels[p].astype(np.complex128), 0.1) for p in range(128)])
+    np.testing.assert_allclose(lam_gpu, lam_ref, rtol=1e-13)
+    seeds = d.derive_seeds(2018, 128).cpu().numpy()
+    lips = d.partition(8).lipschitz if backend == "rbpg" else d.lipschitz()
+    grid = OB.GridDesc(batch.grid.elevation)
+    ref = OB.run(a, batch.pixels, lam_ref, backend, seeds=seeds, grid=grid, k_max=2, lips=lips, max_iters=500, tol=1e-6, num_blocks=8)
+    its = est.solution.iterations.cpu().numpy()
+    order, sup = est.model_order.cpu().numpy(), est.support.cpu().numpy()
+    assert [int(i) for i in its] == [r["iterations"] for r in ref]
+    for p in range(128):
+        assert list(sup[p, : order[p]]) == list(ref[p]["support"]), p
+        np.testing.assert_allclose(est.amplitudes[p, : order[p]].cpu().numpy(), ref[p]["amplitudes"], rtol=1e-6, atol=1e-12)
