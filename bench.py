@@ -7,8 +7,10 @@ lambda rule (0.1 max|A^H b|) -> per-pixel RBPG seeds -> batched solve (max_iters
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--config 2] [--backend rbpg|fista|ista] [--pixels P]
 
-Multi-GPU (torchrun, one rank per GPU): each rank solves its own full batch (pixel ids offset by
-rank, no collective on the data path) -> weak scaling; value = all pixels / max-over-ranks time.
+Multi-GPU (torchrun, one rank per GPU): the ONE batch is pixel-sharded over the ranks (contiguous
+ranges, seeds from the global pixel id, no collective on the data path) -> strong scaling;
+value = the batch's pixels / max-over-ranks time; e2e goes through ``pipeline_sharded`` (ordered
+all-gather of the estimates).
 ``--impl reference`` times the UNMODIFIED reference (``baseline/_ref``, its CLI worker's call
 sequence per pixel, all host cores, process pool as in cli.py:136-144) on a bounded sample; the
 oracle port stands in only when the reference is not installed (oracle/reference_arm.py).
@@ -273,14 +275,17 @@ def run_b200(args):
     from paper_1805_01759_b200.synth import make_config
 
     batch = make_config(args.config, num_pixels=args.pixels)
-    P, n, m = batch.num_pixels, batch.n, batch.m
+    P_total, n, m = batch.num_pixels, batch.n, batch.m
     d = tb.Dictionary(batch.dictionary, device=dev)
     grid = batch.grid
     scfg = tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8, seed=2018)
     pcfg = tb.PipelineConfig(solver=scfg, backend=args.backend, k_max=batch.k_max)
-    first_id = rank * P
-    pix_dev = torch.from_numpy(batch.pixels).to(dev)
-    pix_host = torch.from_numpy(batch.pixels).pin_memory()
+    # ONE batch pixel-sharded over the ranks: contiguous ranges, seeds from the global pixel id
+    first_id, last_id = tb.pixel_shard(P_total, world, rank)
+    P = last_id - first_id
+    pix_dev = torch.from_numpy(batch.pixels[first_id:last_id]).to(dev)
+    pix_all_host = torch.from_numpy(batch.pixels).pin_memory()
+    pix_host = pix_all_host[first_id:last_id]
     # per-dictionary setup (power iterations) outside the timed region, like a resident service
     if args.backend == "rbpg":
         d.partition(scfg.num_blocks)
@@ -327,17 +332,21 @@ def run_b200(args):
     ms = ev0.elapsed_time(ev1)
     kms = [x.elapsed_time(y) for x, y in zip(ks, ke)]
     pix_iters = float(sum(float(x.double().sum().item()) for x in its_list))
+    if world > 1:  # all ranks' pixel-iterations (the roofline is per GPU: / world below)
+        t = torch.tensor([pix_iters], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)
+        pix_iters = float(t.item())
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * P * args.steps / (ms / 1000.0)
+    value = P_total * args.steps / (ms / 1000.0)
 
     # ---- roofline of the dominant kernel (the solver launch), achieved from live CUDA events
     flop_pi = flops_per_pixel_iteration(args.backend, n, m, scfg.num_blocks)
     kernel_ms = float(np.mean(kms))
-    achieved = pix_iters / args.steps * flop_pi / (kernel_ms / 1000.0) / 1e12
+    achieved = pix_iters / world / args.steps * flop_pi / (kernel_ms / 1000.0) / 1e12
     peak, peak_src = fp32_peak()
 
     # ---- end to end through the public API with host buffers (pinned H2D in, D2H results out)
@@ -351,10 +360,15 @@ def run_b200(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        px = pix_host.to(dev, non_blocking=True)
-        est = step(px)
+        if world > 1:
+            # the public multi-GPU entry: this rank's shard from pinned host memory, solve +
+            # select, ordered all-gather (NCCL) of the estimates, rank 0 reads them back
+            est = tb.pipeline_sharded(d, pix_all_host, grid, pcfg, beta=0.1, keep_x=False)
+        else:
+            px = pix_host.to(dev, non_blocking=True)
+            est = step(px)
         outs = [est.model_order, est.support, est.amplitudes, est.elevations, est.solution.objective_final, est.solution.iterations, est.solution.status]
-        host = [o.to("cpu", non_blocking=True) for o in outs]
+        host = [o.to("cpu", non_blocking=True) for o in outs] if rank == 0 else []
         e1.record(stream)
         torch.cuda.synchronize()
         d2h = sum(o.numel() * o.element_size() for o in outs)
@@ -365,20 +379,21 @@ def run_b200(args):
         t = torch.tensor([e2e_step], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step = float(t.item())
-    e2e_value = world * P / (e2e_step / 1000.0)
+    e2e_value = P_total / (e2e_step / 1000.0)
     st = est.solution.status.cpu().numpy()
     its = est.solution.iterations.cpu().numpy()
 
-    traffic, traffic_src = ncu_traffic(f"cfg{args.config}/{args.backend}/{P}")
+    traffic, traffic_src = ncu_traffic(f"cfg{args.config}/{args.backend}/{P_total}")
     line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "c64 (fp64 scalars/residuals)", "data": "synthetic (BASELINE.json config 2 shapes and distributions, seeded)",
             "config": {
-                "workload": f"cfg{args.config}", "n": n, "m": m, "pixels_per_gpu": P, "backend": args.backend, "num_blocks": 8,
-                "max_iters": 500, "tol": 1e-6, "lambda": "0.1*max|A^H b|", "k_max": batch.k_max, "parallelism": f"pixel-sharded x{world}, no collective",
+                "workload": f"cfg{args.config}", "n": n, "m": m, "pixels": P_total, "pixels_per_gpu": P, "backend": args.backend, "num_blocks": 8,
+                "max_iters": 500, "tol": 1e-6, "lambda": "0.1*max|A^H b|", "k_max": batch.k_max,
+                "parallelism": f"one batch pixel-sharded x{world} (contiguous ranges, seeds by global pixel id), no collective on the data path",
                 "l2": "inputs (B = %d MB) and x_hat output exceed the 126 MB L2; no explicit flush" % (P * n * 8 // 2**20),
                 "step": "lambda + seeds + solve + select, whole batch",
             },

@@ -161,3 +161,125 @@ def gather_columns(local_x: list, shard_ranges: list, m: int):
     for x, ranges in zip(local_x, shard_ranges):
         full[:, local_columns(ranges)] = np.asarray(x)
     return full
+
+
+# ------------------------------------------------------------------ pixel-sharded pipeline (cfg1-4)
+
+_EST_FIELDS = ("model_order", "support", "amplitudes", "elevations", "motion_params", "selection_scores", "n_scores", "error")
+_SOL_FIELDS = ("objective_final", "iterations", "status")
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+def _all_gather_rows(t, spans, group):
+    """Ordered all-gather of a per-rank row block (contiguous pixel shards, sizes differ by <= 1).
+    Host plumbing: works on CPU tensors too (gloo), so it is tested without a GPU."""
+    import torch
+
+    dist = _dist()
+    rows = max(e - s for s, e in spans)
+    real = torch.view_as_real(t) if t.is_complex() else t
+    home = real.device
+    if dist.get_backend(group) == "gloo":  # gloo gathers host tensors; NCCL gathers in HBM
+        real = real.cpu()
+    pad = torch.zeros((rows,) + tuple(real.shape[1:]), dtype=real.dtype, device=real.device)
+    pad[: real.shape[0]] = real
+    bufs = [torch.empty_like(pad) for _ in spans]
+    dist.all_gather(bufs, pad, group=group)
+    out = torch.cat([b[: e - s] for b, (s, e) in zip(bufs, spans)]).to(home)
+    return torch.view_as_complex(out) if t.is_complex() else out
+
+
+def gather_estimates(est, num_pixels: int, group=None):
+    """All ranks' contiguous-shard ``BatchEstimates`` -> the whole batch's, in pixel order, on every
+    rank (one all-gather per field over the job's process group: NCCL on GPUs).  The pixel order of
+    the output equals the input order for any world size, as the reference's ordered ``pool.map``
+    output (cli.py:136-144)."""
+    from .slimmer import BatchEstimates
+
+    dist = _dist()
+    world = dist.get_world_size(group)
+    spans = [pixel_shard(num_pixels, world, g) for g in range(world)]
+    fields = {f: _all_gather_rows(getattr(est, f), spans, group) for f in _EST_FIELDS}
+    out = BatchEstimates(**fields)
+    if est.solution is not None:
+        sol = {f: _all_gather_rows(getattr(est.solution, f), spans, group) for f in _SOL_FIELDS}
+        x = _all_gather_rows(est.solution.x_hat, spans, group) if est.solution.x_hat is not None else None
+        out.solution = BatchSolution(x_hat=x, history=None, wall_time=est.solution.wall_time, **sol)
+        out.solution._no_append = getattr(est.solution, "_no_append", False)
+    if est.lam is not None and hasattr(est.lam, "is_complex"):
+        out.lam = _all_gather_rows(est.lam, spans, group)
+    return out
+
+
+def pipeline_sharded(dictionary, pixels, grid, config, beta: float = 0.05, run_seed=None, devices=None, group=None,
+                     gather: bool = True, keep_x: bool = True):
+    """The batched pipeline with the pixel batch sharded over GPUs.
+
+    Pixels are independent, so every GPU solves a contiguous pixel range with NO collective on the
+    data path; per-pixel seeds depend only on the global pixel id (cli.py:102), so every output is
+    bit-identical for any number of GPUs (the reference's worker-count invariance,
+    test_acceptance.py:266-312).
+
+    * ``torch.distributed`` initialised (one process per GPU, e.g. torchrun): this rank takes
+      ``pixel_shard(P, world, rank)`` of ``pixels`` (the whole batch, on the host or any device) and,
+      with ``gather``, the ranks all-gather the estimates in pixel order (the output collection).
+    * otherwise ``devices`` (a list of CUDA devices) shards the batch inside one process: the
+      shards' work is enqueued on every device before any result is collected, so the GPUs run
+      concurrently; results are concatenated on ``devices[0]``.
+    ``dictionary``: the matrix, or a Dictionary per device (a dict device -> Dictionary) to reuse
+    contexts.  Returns BatchEstimates for the whole batch (or, ``gather=False``, this rank's shard).
+    """
+    from .slimmer import BatchEstimates, pipeline_batch
+
+    torch = _torch()
+    p = int(pixels.shape[0])
+    seed = config.solver.seed if run_seed is None else run_seed
+    dist = _dist()
+
+    def norm(dev):
+        if dev is None:
+            return torch.device("cuda", torch.cuda.current_device())
+        return dev if isinstance(dev, torch.device) else torch.device("cuda", int(dev))
+
+    def ctx(dev):
+        dev = norm(dev)
+        if isinstance(dictionary, dict):
+            return dictionary[dev.index] if dev.index in dictionary else dictionary[dev]
+        if isinstance(dictionary, Dictionary):
+            if dev != dictionary.device:
+                raise ConfigurationError("a single Dictionary can only serve its own device")
+            return dictionary
+        return Dictionary(dictionary, device=dev)
+
+    def shard(rows):
+        s, e = rows
+        return pixels[s:e]
+
+    if dist is not None:
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        s, e = pixel_shard(p, world, rank)
+        est = pipeline_batch(ctx(None), shard((s, e)), grid, config, beta=beta, run_seed=seed, first_pixel_id=s)
+        if not keep_x:
+            est.solution.x_hat = None
+        return gather_estimates(est, p, group) if gather else est
+    devs = [norm(x) for x in (devices or [None])]
+    spans = [pixel_shard(p, len(devs), g) for g in range(len(devs))]
+    parts = []
+    for dev, (s, e) in zip(devs, spans):  # enqueue every shard before touching any result
+        with torch.cuda.device(dev):
+            parts.append(pipeline_batch(ctx(dev), shard((s, e)), grid, config, beta=beta, run_seed=seed, first_pixel_id=s))
+    home = devs[0]
+    cat = lambda ts: torch.cat([t.to(home) for t in ts])  # noqa: E731
+    out = BatchEstimates(**{f: cat([getattr(q, f) for q in parts]) for f in _EST_FIELDS})
+    sols = [q.solution for q in parts]
+    out.solution = BatchSolution(x_hat=cat([q.x_hat for q in sols]) if keep_x else None, history=None,
+                                 wall_time=max(q.wall_time for q in sols), **{f: cat([getattr(q, f) for q in sols]) for f in _SOL_FIELDS})
+    out.solution._no_append = getattr(sols[0], "_no_append", False)
+    if all(hasattr(q.lam, "is_complex") for q in parts):
+        out.lam = cat([q.lam for q in parts])
+    return out

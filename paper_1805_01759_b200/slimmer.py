@@ -10,8 +10,7 @@ estimate_params kernel, all on one stream with no host round trip between stages
 from __future__ import annotations
 
 import ctypes
-import time
-from dataclasses import dataclass, field, replace
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -206,5 +205,3 @@ def estimates_to_record(pixel_id: int, est: ScattererEstimates) -> dict:
         "support": [int(v) for v in est.support],
     }
 
-
-_ = (replace, time)

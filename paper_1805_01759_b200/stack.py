@@ -17,7 +17,6 @@ import csv
 import datetime
 import hashlib
 import json
-from pathlib import Path
 
 import numpy as np
 
@@ -152,9 +151,17 @@ def _sha256(path) -> str:
     return h.hexdigest()
 
 
-def solve_stack(stack_path, grid_dict: dict, pipe_config, seed: int | None = None, out_jsonl=None, out_csv=None, beta: float = 0.05):
-    """Batched equivalent of ``tomobpdn solve`` (cli.py:112-174); returns the ordered records."""
+def solve_stack(stack_path, grid_dict: dict, pipe_config, seed: int | None = None, out_jsonl=None, out_csv=None, beta: float = 0.05,
+                group=None):
+    """Batched equivalent of ``tomobpdn solve`` (cli.py:112-174); returns the ordered records.
+
+    Under ``torch.distributed`` (one process per GPU, e.g. torchrun) the stack's pixels are sharded
+    in contiguous ranges over the ranks (no collective on the data path; seeds from the global pixel
+    id, cli.py:102), the records are all-gathered in pixel order and rank 0 writes the outputs, so
+    the JSONL/CSV bytes are identical for any number of GPUs (test_acceptance.py:266-312).
+    """
     from . import __version__
+    from .sharded import _dist, pixel_shard
     from .slimmer import estimates_to_record, pipeline_batch
     from .solver import Dictionary
 
@@ -163,15 +170,23 @@ def solve_stack(stack_path, grid_dict: dict, pipe_config, seed: int | None = Non
     seed = pipe_config.solver.seed if seed is None else seed
     a = build_steering_matrix(geometry.spatial_frequencies(), grid, eta=geometry.temporal_frequencies(grid.motion_bases), sign=1.0)
     d = Dictionary(a)
+    dist = _dist()
+    world = dist.get_world_size(group) if dist is not None else 1
+    rank = dist.get_rank(group) if dist is not None else 0
+    start, stop = pixel_shard(pixels.shape[0], world, rank)
     records = []
-    if pixels.shape[0]:
-        est = pipeline_batch(d, pixels, grid, pipe_config, beta=beta, run_seed=seed)
-        for i in range(pixels.shape[0]):
+    if stop > start:
+        est = pipeline_batch(d, pixels[start:stop], grid, pipe_config, beta=beta, run_seed=seed, first_pixel_id=start)
+        for i in range(stop - start):
             try:
-                records.append(estimates_to_record(i, est.estimates(i)))
+                records.append(estimates_to_record(start + i, est.estimates(i)))
             except Exception as exc:  # per-pixel error record (cli.py:104-108)
-                records.append({"pixel_id": i, "error": str(exc)})
-    if out_jsonl is not None:
+                records.append({"pixel_id": start + i, "error": str(exc)})
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, records, group=group)
+        records = [r for part in parts for r in part]
+    if out_jsonl is not None and rank == 0:
         with open(out_jsonl, "w", encoding="utf-8", newline="\n") as fh:
             for r in records:
                 fh.write(json.dumps(r, separators=(",", ":")))
@@ -198,5 +213,3 @@ def solve_stack(stack_path, grid_dict: dict, pipe_config, seed: int | None = Non
             fh.write("\n")
     return records
 
-
-_ = Path

@@ -68,3 +68,43 @@ def test_column_sharded_reduction_gloo_world2():
     out = mgr.dict()
     mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
     assert dict(out) == {0: 1, 1: 1}
+
+
+def _gather_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_01759_b200.sharded import gather_estimates
+    from paper_1805_01759_b200.slimmer import BatchEstimates
+    from paper_1805_01759_b200.solver import BatchSolution
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p, k = 7, 2
+    s, e = pixel_shard(p, world, rank)
+    ids = torch.arange(s, e)
+    est = BatchEstimates(
+        model_order=ids.to(torch.int32), support=torch.stack([ids, -ids], 1), amplitudes=(ids[:, None] * (1 + 2j)).repeat(1, k).to(torch.complex128),
+        elevations=ids[:, None].double().repeat(1, k), motion_params=torch.zeros(e - s, k, 0, dtype=torch.float64),
+        selection_scores=ids[:, None].double().repeat(1, k + 1), n_scores=ids.to(torch.int32), error=torch.zeros(e - s, dtype=torch.int32),
+    )
+    est.solution = BatchSolution(x_hat=(ids[:, None] * 1j).repeat(1, 3).to(torch.complex64), objective_final=ids.double(), iterations=ids.to(torch.int32), status=ids.to(torch.int32) % 4)
+    full = gather_estimates(est, p)
+    want = torch.arange(p)
+    ok = torch.equal(full.model_order, want.to(torch.int32)) and torch.equal(full.support[:, 1], -want)
+    ok = ok and torch.equal(full.amplitudes[:, 0], (want * (1 + 2j)).to(torch.complex128)) and torch.equal(full.solution.x_hat[:, 2], (want * 1j).to(torch.complex64))
+    ok = ok and torch.equal(full.solution.objective_final, want.double()) and full.motion_params.shape == (p, k, 0)
+    out[rank] = int(ok)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_estimates_ordered_gloo(world):
+    """Ordered all-gather of ragged contiguous pixel shards (7 pixels over 2 or 3 ranks)."""
+    port = 29700 + (os.getpid() % 200) + world
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gather_worker, args=(world, port, out), nprocs=world, join=True)
+    assert dict(out) == {g: 1 for g in range(world)}
