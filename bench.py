@@ -265,8 +265,8 @@ def run_b200(args):
 
     world, rank, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))  # gloo: multi-rank smoke on one GPU
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -432,8 +432,8 @@ def run_cfg5_sharded(args):
 
     world, rank, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))  # gloo: multi-rank smoke on one GPU
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
