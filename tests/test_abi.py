@@ -51,11 +51,25 @@ def test_ctypes_signatures_cover_header(lib):
         assert len(params) == len(args), (name, len(params), len(args))
 
 
-def test_config_struct_layout():
+def test_config_struct_layout(tmp_path):
+    """The ctypes mirror of tb_solver_config has the C compiler's size and field offsets."""
+    import subprocess
+
     from paper_1805_01759_b200 import _lib
 
-    assert ctypes.sizeof(_lib.SolverConfigC) == 4 * 4 + 3 * 8
-    assert _lib.SolverConfigC.tol.offset == 16
+    fields = [f for f, _ in _lib.SolverConfigC._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stddef.h>\n#include <stdio.h>\n#include "tomobpdn_b200.h"\nint main(void) {\n'
+        + '  printf("%zu\\n", sizeof(tb_solver_config));\n'
+        + "".join(f'  printf("%zu\\n", offsetof(tb_solver_config, {f}));\n' for f in fields)
+        + "  return 0;\n}\n"
+    )
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert ctypes.sizeof(_lib.SolverConfigC) == vals[0]
+    assert [getattr(_lib.SolverConfigC, f).offset for f in fields] == vals[1:]
 
 
 def test_version_and_errors_without_gpu(lib):
