@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
   double2* xs = DC ? rv + n : apv + n;           // x (fp64 iterate)
   double2* zs = xs + m;                          // broadcast buffer for forward products [max_width]
   float4* ryv = reinterpret_cast<float4*>(zs + P.max_width);  // r_y rounded, as (r.x, r.y, r.y, -r.x)
+  float2* ry2 = reinterpret_cast<float2*>(ryv);                // DC: r_y rounded, as (r.x, r.y)
   double2* ds = reinterpret_cast<double2*>(ryv + n);  // d = x - prev, fp64 (y = x + m_k d); not DC
   float2* bv = reinterpret_cast<float2*>(ds + m);  // b; not RBPG
   double2* dlt = reinterpret_cast<double2*>(ryv + n);  // DC: delta [J][n]
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           if (i < n) {
             const double2 r = rv[i], dl = dlt[blk * n + i];
             ry[q] = make_double2(fma(mk, dl.x, r.x), fma(mk, dl.y, r.y));
-            ryv[i] = conj_operand((float)ry[q].x, (float)ry[q].y);
+            ry2[i] = make_float2((float)ry[q].x, (float)ry[q].y);
           }
         }
       } else if (RB) {
@@ -353,8 +354,11 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
         const int passes = (width + 31) >> 5;
-        adjoint_dispatch<1, MAXT, ASMEM, CM>(passes, acc, CM ? As + (size_t)(cs + lane) * ns : (ASMEM ? As : P.A) + cs + lane, ASMEM ? ms : m,
-                                         CM ? 32 * ns : 32, ryv, n, lane + 32 * (passes - 1) < width);
+        const float2* ap = CM ? As + (size_t)(cs + lane) * ns : (ASMEM ? As : P.A) + cs + lane;
+        if (DC)
+          adjoint_dispatch2<1, MAXT, ASMEM, CM>(passes, acc, ap, ASMEM ? ms : m, CM ? 32 * ns : 32, ry2, n, lane + 32 * (passes - 1) < width);
+        else
+          adjoint_dispatch<1, MAXT, ASMEM, CM>(passes, acc, ap, ASMEM ? ms : m, CM ? 32 * ns : 32, ryv, n, lane + 32 * (passes - 1) < width);
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) g[t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
       }

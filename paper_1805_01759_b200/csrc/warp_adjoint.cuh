@@ -44,4 +44,67 @@ __device__ __forceinline__ void adjoint_dispatch(int passes, float2* acc, const 
   }
 }
 
+// c += (a, a) * r: one packed FFMA2 with a scalar broadcast operand
+__device__ __forceinline__ void ffma2_bcast(float2& c, float a, float2 r) {
+  asm("{\n\t.reg .b64 cc, aa, rr;\n\t"
+      "mov.b64 cc, {%0, %1};\n\t"
+      "mov.b64 aa, {%2, %2};\n\t"
+      "mov.b64 rr, {%3, %4};\n\t"
+      "fma.rn.f32x2 cc, aa, rr, cc;\n\t"
+      "mov.b64 {%0, %1}, cc;\n\t}"
+      : "+f"(c.x), "+f"(c.y)
+      : "f"(a), "f"(r.x), "f"(r.y));
+}
+
+// RBPG form of the column-lane adjoint: r_y is stored as plain (r.x, r.y) pairs (one 8-byte
+// broadcast per row instead of the 16-byte (r.x, r.y, r.y, -r.x) quad: the quad load costs two
+// shared-memory wavefronts, and the r_y broadcasts were 23% of the kernel's shared wavefronts), and
+// each pass keeps two independent packed accumulators, p += a.x r and q += a.y r, combined once:
+// conj(a) r summed over rows = (p.x + q.y, p.y - q.x).  Rows are still summed in order.
+template <int NP, bool ASMEM, bool CM>
+__device__ __forceinline__ void adjoint_passes2(float2* acc, const float2* ap, int stride, int pstride, const float2* ry2, int n, bool last) {
+  const int rs = CM ? 1 : stride;
+  float2 p[NP], q[NP];
+#pragma unroll
+  for (int t = 0; t < NP; ++t) p[t] = q[t] = make_float2(0.f, 0.f);
+  int i = 0;
+#pragma unroll 1
+  for (; i + 8 <= n; i += 8, ap += 8 * rs) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float2 r = ry2[i + u];
+#pragma unroll
+      for (int t = 0; t < NP; ++t)
+        if (t < NP - 1 || last) {
+          const float2 a = ASMEM ? ap[u * rs + t * pstride] : __ldg(ap + u * rs + t * pstride);
+          ffma2_bcast(p[t], a.x, r);
+          ffma2_bcast(q[t], a.y, r);
+        }
+    }
+  }
+#pragma unroll 1
+  for (; i < n; ++i, ap += rs) {
+    const float2 r = ry2[i];
+#pragma unroll
+    for (int t = 0; t < NP; ++t)
+      if (t < NP - 1 || last) {
+        const float2 a = ASMEM ? ap[t * pstride] : __ldg(ap + t * pstride);
+        ffma2_bcast(p[t], a.x, r);
+        ffma2_bcast(q[t], a.y, r);
+      }
+  }
+#pragma unroll
+  for (int t = 0; t < NP; ++t) acc[t] = make_float2(p[t].x + q[t].y, p[t].y - q[t].x);
+}
+template <int NP, int MAXT, bool ASMEM, bool CM>
+__device__ __forceinline__ void adjoint_dispatch2(int passes, float2* acc, const float2* ap, int stride, int pstride, const float2* ry2, int n, bool last) {
+  if constexpr (NP <= MAXT) {
+    if (passes == NP) {
+      adjoint_passes2<NP, ASMEM, CM>(acc, ap, stride, pstride, ry2, n, last);
+      return;
+    }
+    adjoint_dispatch2<NP + 1, MAXT, ASMEM, CM>(passes, acc, ap, stride, pstride, ry2, n, last);
+  }
+}
+
 }  // namespace tb
