@@ -145,7 +145,7 @@ def ncu_traffic(key: str):
         return None, None
 
 
-def measure_cpu(batch, backend, k_max, cores, gpu_mean_iters, cfg_id, sample=None, hoist=False, min_wall=8.0):
+def measure_cpu(batch, backend, k_max, cores, gpu_mean_iters, cfg_id, sample=None, hoist=False, min_wall=8.0, setup=None):
     """Reference CPU throughput (px/s) on this host's cores -> (value, cpu_baseline dict).
 
     The unmodified reference (oracle/reference_arm.py: baseline/_ref, its own CLI-worker call
@@ -155,7 +155,8 @@ def measure_cpu(batch, backend, k_max, cores, gpu_mean_iters, cfg_id, sample=Non
     solve takes minutes to hours): the iteration cost t_I is timed on a few fixed iterations with
     the per-dictionary setup hoisted (computed once by the reference's own functions), the setup
     t_S is timed once on one core, and a whole solve is charged t_S + (GPU mean iterations) t_I
-    core-seconds (cfg5: t_S is reported separately, not charged).
+    core-seconds (cfg5: t_S is reported separately, not charged, and the hoisted setup is the GPU's
+    fp64 power-iteration result passed in ``setup``, since the reference's takes minutes).
     """
     from oracle import reference_arm as R
 
@@ -191,8 +192,9 @@ def measure_cpu(batch, backend, k_max, cores, gpu_mean_iters, cfg_id, sample=Non
                 f"process pool x{cores}, {wall:.1f} s wall")
     else:
         fixed = 10 if cfg_id == 4 else 2
-        count = sample or (cores if cfg_id == 4 else min(cores, P))
-        pool = R.ReferencePool(batch.dictionary, batch.grid, backend, k_max, min(cores, count), hoist=True, fixed_iters=fixed)
+        # cfg5: two RHS on two workers (each worker holds its own 1.7 GB complex128 dictionary)
+        count = sample or (cores if cfg_id == 4 else min(2, P))
+        pool = R.ReferencePool(batch.dictionary, batch.grid, backend, k_max, min(cores, count), hoist=True, setup=setup, fixed_iters=fixed)
         try:
             idx = np.arange(count) % P
             wall, _ = pool.run(idx, batch.pixels[idx], chunksize=1)
@@ -529,7 +531,9 @@ def run_cfg5_sharded(args):
         line["roofline"]["frac"] = achieved / world / peak
         if not args.no_cpu_baseline and world == 1:
             cores = os.cpu_count() or 1
-            _, line["cpu_baseline"] = measure_cpu(batch, args.backend, batch.k_max, cores, float(its.mean()), 5, sample=args.cpu_sample, hoist=True)
+            part = full.partition(8) if args.backend == "rbpg" else None
+            setup = ("blocks", (part.blocks, part.lipschitz)) if part is not None else ("lipschitz", full.lipschitz() / 2.0)
+            _, line["cpu_baseline"] = measure_cpu(batch, args.backend, batch.k_max, cores, float(its.mean()), 5, sample=args.cpu_sample, hoist=True, setup=setup)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -70,6 +70,8 @@ def _init(path, a, elevation, motion_axes, motion_bases, backend, k_max, run_see
 
     if setup is not None:
         kind, value = setup
+        if kind == "blocks":  # (blocks, lipschitz) computed elsewhere (the GPU's fp64 power iterations)
+            kind, value = "partition", T.BlockPartition(blocks=tuple(tuple(b) for b in value[0]), lipschitz=np.asarray(value[1], float))
         if kind == "partition":
             S.block_partition = lambda l_total, num_blocks, mat, _p=value: _p
         else:
@@ -103,15 +105,20 @@ def _setup_value(path, a, backend, num_blocks):
 class ReferencePool:
     """A warm process pool running the reference pipeline; ``run(ids, pixels)`` returns wall seconds."""
 
-    def __init__(self, dictionary, grid, backend, k_max, workers, run_seed=2018, beta=0.1, hoist=False, **solver_kw):
+    def __init__(self, dictionary, grid, backend, k_max, workers, run_seed=2018, beta=0.1, hoist=False, setup=None, **solver_kw):
         self.path = locate()
         if self.path is None:
             raise RuntimeError("reference package not found (baseline/_ref or /root/reference/pkg/src)")
         a = np.asarray(dictionary).astype(np.complex128)
         kw = dict(max_iters=500, tol=1e-6, num_blocks=8)
         kw.update(solver_kw)
-        setup = _setup_value(self.path, a, backend, kw["num_blocks"]) if hoist else None
-        self.setup_s = None
+        # setup: None -> computed here by the reference's own functions; or ("blocks", (blocks,
+        # lipschitz)) / ("lipschitz", value) supplied by the caller (bench.py passes the GPU's fp64
+        # power-iteration results for cfg5, whose reference setup takes minutes)
+        if hoist and setup is None:
+            setup = _setup_value(self.path, a, backend, kw["num_blocks"])
+        elif not hoist:
+            setup = None
         self.workers = workers
         args = (self.path, a, np.asarray(grid.elevation, float), tuple(np.asarray(x, float) for x in grid.motion_axes),
                 tuple(getattr(grid, "motion_bases", ()) or ()), backend, k_max, run_seed, beta, kw, setup)
