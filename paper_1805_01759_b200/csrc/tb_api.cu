@@ -46,14 +46,17 @@ struct tb_ctx {
   // are only freed / reallocated after `done` has completed.
   cudaEvent_t done = nullptr;
   cudaStream_t last = nullptr;
+  bool capturing = false;  // inside a graph capture of the tiled rounds: ordering handled around it
 };
 
 // Order `st` after the previous user of the context's mutable state (see tb_ctx::done).
 static cudaError_t ctx_acquire(tb_ctx* c, cudaStream_t st) {
+  if (c->capturing) return cudaSuccess;
   if (c->done && c->last != st) return cudaStreamWaitEvent(st, c->done, 0);
   return cudaSuccess;
 }
 static cudaError_t ctx_release(tb_ctx* c, cudaStream_t st) {
+  if (c->capturing) return cudaSuccess;
   c->last = st;
   return cudaEventRecord(c->done, st);
 }
@@ -125,6 +128,13 @@ static int fail(int code, const char* fmt, ...) {
 
 static std::atomic<long long> g_launches{0};
 void tb::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// TB_TILED_GRAPH=0 disables the CUDA-graph replay of the tiled round loop (A/B)
+static bool tiled_use_graph() {
+  const char* e = getenv("TB_TILED_GRAPH");
+  return !(e && *e && atoi(e) == 0);
+}
 
 extern "C" {
 
@@ -637,6 +647,82 @@ int tb_tiled_destroy(tb_tiled* h) {
   return TB_OK;
 }
 
+// The tiled solver's round loop as CUDA-graph replays: GRAPH_ROUNDS rounds (each the prep, schedule,
+// pass, reduce, update[, commit] launches) are captured once per handle on a private stream -- every
+// kernel reads its per-round work from device state (pending pixels, tiles), so the same graph is
+// valid for the whole solve -- and replayed until the device-side count of unfinished pixels reaches
+// 0 (polled once per replay, as the stream loop polls every 16 rounds; rounds past the last pixel
+// are no-ops).  Removes the host launch overhead of ~7 launches per round (cfg5 RBPG: ~3,500 rounds).
+static constexpr int GRAPH_ROUNDS = 16;
+static int run_rounds_graph(tb_tiled* h, long long max_rounds, int total, cudaStream_t st) {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  int rc = TB_OK;
+  auto cleanup = [&]() {
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    if (ev) cudaEventDestroy(ev);
+    if (cs) cudaStreamDestroy(cs);
+  };
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, st);  // the capture stream starts after the caller's work
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev, 0);
+  if (e == cudaSuccess) e = ctx_acquire(h->ctx, cs);  // after the context's previous user
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(TB_ERR_CUDA, "graph setup: %s", cudaGetErrorString(e));
+  }
+  const long long before = tb_launch_count();
+  e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(TB_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  }
+  h->ctx->capturing = true;
+  for (int r = 0; r < GRAPH_ROUNDS && rc == TB_OK; ++r) {
+    rc = tb_tiled_round_a(h, cs);
+    if (rc == TB_OK) rc = tb_tiled_round_b(h, cs);
+  }
+  h->ctx->capturing = false;
+  const cudaError_t ee = cudaStreamEndCapture(cs, &g);
+  if (rc != TB_OK || ee != cudaSuccess) {
+    cleanup();
+    return rc != TB_OK ? rc : fail(TB_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ee));
+  }
+  const long long per_replay = tb_launch_count() - before;  // kernels in one replay
+  count_launches(-per_replay);                               // captured, not launched
+  h->rounds -= GRAPH_ROUNDS;
+  e = cudaGraphInstantiate(&ge, g, 0);
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(TB_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  }
+  int* rem_h = nullptr;
+  e = cudaMallocHost((void**)&rem_h, sizeof(int));
+  for (long long r = 0; e == cudaSuccess && r < max_rounds; r += GRAPH_ROUNDS) {
+    e = cudaGraphLaunch(ge, cs);
+    if (e != cudaSuccess) break;
+    count_launches(per_replay);
+    h->rounds += GRAPH_ROUNDS;
+    if (r + GRAPH_ROUNDS >= total) {  // poll the device-side count once per replay
+      e = cudaMemcpyAsync(rem_h, h->T.remaining, sizeof(int), cudaMemcpyDeviceToHost, cs);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+      if (e == cudaSuccess && *rem_h == 0) break;
+    }
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(ev, cs);  // the caller's stream continues after the rounds
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev, 0);
+  if (e == cudaSuccess) e = ctx_release(h->ctx, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (rem_h) cudaFreeHost(rem_h);
+  cleanup();
+  if (e != cudaSuccess) return fail(TB_ERR_CUDA, "graph replay: %s", cudaGetErrorString(e));
+  return TB_OK;
+}
+
 static int solve_tiled(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void* pixels, const double* lam,
                        const uint64_t* seeds, int64_t P, void* x, double* f_final, double* hist, int64_t hist_stride,
                        int32_t* iters, int32_t* status, cudaStream_t st) {
@@ -656,17 +742,25 @@ static int solve_tiled(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, c
                              hist ? hist + p0 * hist_stride : nullptr, hist_stride, nullptr, st, &h);
     if (rc != TB_OK) return rc;
     const long long max_rounds = (long long)total * (cfg->backtrack_cap + 1) + 1;
-    for (long long r = 0; r < max_rounds; ++r) {
-      rc = tb_tiled_round_a(h, st);
-      if (rc == TB_OK) rc = tb_tiled_round_b(h, st);
+    if (tiled_use_graph()) {
+      rc = run_rounds_graph(h, max_rounds, total, st);
       if (rc != TB_OK) {
         tb_tiled_destroy(h);
         return rc;
       }
-      if ((r + 1) % 16 == 0 || r + 1 >= total) {
-        int64_t rem = 0;
-        rc = tb_tiled_remaining(h, &rem, st);
-        if (rc != TB_OK || rem == 0) break;
+    } else {
+      for (long long r = 0; r < max_rounds; ++r) {
+        rc = tb_tiled_round_a(h, st);
+        if (rc == TB_OK) rc = tb_tiled_round_b(h, st);
+        if (rc != TB_OK) {
+          tb_tiled_destroy(h);
+          return rc;
+        }
+        if ((r + 1) % 16 == 0 || r + 1 >= total) {
+          int64_t rem = 0;
+          rc = tb_tiled_remaining(h, &rem, st);
+          if (rc != TB_OK || rem == 0) break;
+        }
       }
     }
     rc = tb_tiled_finish(h, (float2*)x + p0 * c->m, f_final + p0, iters + p0, status + p0, st);
