@@ -43,7 +43,7 @@
 
 namespace tb {
 
-template <bool RB, int MAXT, int MAXQ, bool ASMEM>
+template <bool RB, int MAXT, int MAXQ, bool ASMEM, bool SHFL>
 __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) warp_solver_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           if (i < n) {
             const double2 r = rv[i], dl = dlt[blk * n + i];
             ry[q] = make_double2(fma(mk, dl.x, r.x), fma(mk, dl.y, r.y));
-            ry2[i] = make_float2((float)ry[q].x, (float)ry[q].y);
+            if (!SHFL) ry2[i] = make_float2((float)ry[q].x, (float)ry[q].y);
           }
         }
       } else if (RB) {
@@ -355,7 +355,12 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
         const int passes = (width + 31) >> 5;
         const float2* ap = CM ? As + (size_t)(cs + lane) * ns : (ASMEM ? As : P.A) + cs + lane;
-        if (DC)
+        if (DC && SHFL) {
+          float2 ryr[MAXQ];
+#pragma unroll
+          for (int q = 0; q < MAXQ; ++q) ryr[q] = make_float2((float)ry[q].x, (float)ry[q].y);
+          adjoint_dispatch_shfl<1, MAXT, MAXQ, ASMEM, CM>(passes, acc, ap, ASMEM ? ms : m, CM ? 32 * ns : 32, ryr, n, lane + 32 * (passes - 1) < width);
+        } else if (DC)
           adjoint_dispatch2<1, MAXT, ASMEM, CM>(passes, acc, ap, ASMEM ? ms : m, CM ? 32 * ns : 32, ry2, n, lane + 32 * (passes - 1) < width);
         else
           adjoint_dispatch<1, MAXT, ASMEM, CM>(passes, acc, ap, ASMEM ? ms : m, CM ? 32 * ns : 32, ryv, n, lane + 32 * (passes - 1) < width);
@@ -585,8 +590,9 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
 }
 
 template <bool RB, int MAXT, int MAXQ, bool ASMEM>
-static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int grid, cudaStream_t st) {
-  auto k = warp_solver_kernel<RB, MAXT, MAXQ, ASMEM>;
+static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int grid, cudaStream_t st, bool shfl) {
+  // r_y from shuffles only for RBPG (DC) batches smaller than the resident slots (see warp_adjoint.cuh)
+  auto k = (RB && TB_WS_DCACHE && shfl) ? warp_solver_kernel<RB, MAXT, MAXQ, ASMEM, true> : warp_solver_kernel<RB, MAXT, MAXQ, ASMEM, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   count_launch();
@@ -595,22 +601,22 @@ static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int gr
 }
 
 template <bool RB, int MAXT, bool ASMEM>
-static cudaError_t launch_q(const SolveParams& P, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
+static cudaError_t launch_q(const SolveParams& P, int maxq, int warps, size_t smem, int grid, cudaStream_t st, bool shfl) {
   switch (maxq) {
-    case 1: return launch_t<RB, MAXT, 1, ASMEM>(P, warps, smem, grid, st);
-    case 2: return launch_t<RB, MAXT, 2, ASMEM>(P, warps, smem, grid, st);
-    case 4: return launch_t<RB, MAXT, 4, ASMEM>(P, warps, smem, grid, st);
+    case 1: return launch_t<RB, MAXT, 1, ASMEM>(P, warps, smem, grid, st, shfl);
+    case 2: return launch_t<RB, MAXT, 2, ASMEM>(P, warps, smem, grid, st, shfl);
+    case 4: return launch_t<RB, MAXT, 4, ASMEM>(P, warps, smem, grid, st, shfl);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <bool RB, bool ASMEM>
-static cudaError_t launch_tq(const SolveParams& P, int maxt, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
-  if (maxt <= 2) return launch_q<RB, 2, ASMEM>(P, maxq, warps, smem, grid, st);
-  if (maxt <= 4) return launch_q<RB, 4, ASMEM>(P, maxq, warps, smem, grid, st);
-  if (maxt <= 8) return launch_q<RB, 8, ASMEM>(P, maxq, warps, smem, grid, st);
-  if (maxt <= 12) return launch_q<RB, 12, ASMEM>(P, maxq, warps, smem, grid, st);
-  if (maxt <= 16) return launch_q<RB, 16, ASMEM>(P, maxq, warps, smem, grid, st);
+static cudaError_t launch_tq(const SolveParams& P, int maxt, int maxq, int warps, size_t smem, int grid, cudaStream_t st, bool shfl) {
+  if (maxt <= 2) return launch_q<RB, 2, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
+  if (maxt <= 4) return launch_q<RB, 4, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
+  if (maxt <= 8) return launch_q<RB, 8, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
+  if (maxt <= 12) return launch_q<RB, 12, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
+  if (maxt <= 16) return launch_q<RB, 16, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
   return cudaErrorInvalidValue;
 }
 
@@ -648,7 +654,8 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   // a batch smaller than the resident slots (cfg1: 1,024 pixels vs 148 x 16) is spread over every SM
   // with fewer warps each, instead of filling ceil(P / warps) SMs: each pixel's warp then shares its
   // SM's issue slots and shared-memory pipe with fewer others (the batch time is the slowest pixel's)
-  if (P.num_pixels < (long long)num_sms * warps) warps = (int)((P.num_pixels + num_sms - 1) / num_sms);
+  const bool spread = P.num_pixels < (long long)num_sms * warps;
+  if (spread) warps = (int)((P.num_pixels + num_sms - 1) / num_sms);
   if (warps < 1) warps = 1;
   size_t smem = (asmem ? a_bytes : 0) + tables + (size_t)warps * slot;
   long long need = (P.num_pixels + warps - 1) / warps;
@@ -657,8 +664,8 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   if (grid < 1) grid = 1;
   if (used_warps) *used_warps = warps;
   const bool rb = P.mode == SOLVER_RBPG;
-  if (rb) return asmem ? launch_tq<true, true>(P, maxt, maxq, warps, smem, grid, st) : launch_tq<true, false>(P, maxt, maxq, warps, smem, grid, st);
-  return asmem ? launch_tq<false, true>(P, maxt, maxq, warps, smem, grid, st) : launch_tq<false, false>(P, maxt, maxq, warps, smem, grid, st);
+  if (rb) return asmem ? launch_tq<true, true>(P, maxt, maxq, warps, smem, grid, st, spread) : launch_tq<true, false>(P, maxt, maxq, warps, smem, grid, st, spread);
+  return asmem ? launch_tq<false, true>(P, maxt, maxq, warps, smem, grid, st, false) : launch_tq<false, false>(P, maxt, maxq, warps, smem, grid, st, false);
 }
 
 }  // namespace tb

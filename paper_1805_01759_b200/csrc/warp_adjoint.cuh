@@ -107,4 +107,61 @@ __device__ __forceinline__ void adjoint_dispatch2(int passes, float2* acc, const
   }
 }
 
+// Variant of adjoint_passes2 taking r_y from registers: lane i holds row i + 32 q in ryr[q] (the
+// lane = row layout of the residual step), broadcast per row with two shuffles instead of a shared
+// load.  Measured: shuffles compete with the shared loads for the same MIO path, so this is slower
+// when the SM is full of warps (cfg2 139 vs 127 ms) and faster when few warps share an SM and
+// latency dominates (cfg1, 1,024 pixels: 1.08 vs 1.23 ms); the launcher picks it for batches
+// smaller than the resident slots.
+template <int NP, int MAXQ, bool ASMEM, bool CM>
+__device__ __forceinline__ void adjoint_passes_shfl(float2* acc, const float2* ap, int stride, int pstride, const float2* ryr, int n, bool last) {
+  const int rs = CM ? 1 : stride;
+  float2 p[NP], q[NP];
+#pragma unroll
+  for (int t = 0; t < NP; ++t) p[t] = q[t] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int h = 0; h < MAXQ; ++h) {
+    const int i0 = 32 * h, i1 = min(n, 32 * h + 32);
+    const float rx = ryr[h].x, ry = ryr[h].y;
+    int i = i0;
+#pragma unroll 1
+    for (; i + 8 <= i1; i += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float2 r = make_float2(__shfl_sync(TB_FULL_MASK, rx, i + u - i0), __shfl_sync(TB_FULL_MASK, ry, i + u - i0));
+#pragma unroll
+        for (int t = 0; t < NP; ++t)
+          if (t < NP - 1 || last) {
+            const float2 a = ASMEM ? ap[(i + u) * rs + t * pstride] : __ldg(ap + (i + u) * rs + t * pstride);
+            ffma2_bcast(p[t], a.x, r);
+            ffma2_bcast(q[t], a.y, r);
+          }
+      }
+    }
+#pragma unroll 1
+    for (; i < i1; ++i) {
+      const float2 r = make_float2(__shfl_sync(TB_FULL_MASK, rx, i - i0), __shfl_sync(TB_FULL_MASK, ry, i - i0));
+#pragma unroll
+      for (int t = 0; t < NP; ++t)
+        if (t < NP - 1 || last) {
+          const float2 a = ASMEM ? ap[i * rs + t * pstride] : __ldg(ap + i * rs + t * pstride);
+          ffma2_bcast(p[t], a.x, r);
+          ffma2_bcast(q[t], a.y, r);
+        }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NP; ++t) acc[t] = make_float2(p[t].x + q[t].y, p[t].y - q[t].x);
+}
+template <int NP, int MAXT, int MAXQ, bool ASMEM, bool CM>
+__device__ __forceinline__ void adjoint_dispatch_shfl(int passes, float2* acc, const float2* ap, int stride, int pstride, const float2* ryr, int n, bool last) {
+  if constexpr (NP <= MAXT) {
+    if (passes == NP) {
+      adjoint_passes_shfl<NP, MAXQ, ASMEM, CM>(acc, ap, stride, pstride, ryr, n, last);
+      return;
+    }
+    adjoint_dispatch_shfl<NP + 1, MAXT, MAXQ, ASMEM, CM>(passes, acc, ap, stride, pstride, ryr, n, last);
+  }
+}
+
 }  // namespace tb
