@@ -234,6 +234,33 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
         for (int j = 0; j < 4; ++j)
           if (cg + 16 * j < ncols) acc[q][j] = g[cg + 16 * j];
       }
+    } else if (count <= 8) {
+      // few-RHS tiles (cfg5 RBPG: ~8 RHS per block per round): the (column, pixel pair) items are
+      // spread over ALL 256 threads -- 64 columns x 4 pairs, one column each -- instead of leaving
+      // the 12 pixel-pair rows of the 16 x 16 mapping idle; results go through shared memory (the
+      // candidate tile's space, consumed before the epilogue writes it).  Same per-pixel row order
+      // and fmaf sequence as below, so bit-identical.
+      float2* sG = reinterpret_cast<float2*>(sZ);  // [8][TL_CT]
+      const int c = tid & (TL_CT - 1), pp = tid / TL_CT;
+      if (2 * pp < count) {
+        float2 g0 = make_float2(0.f, 0.f), g1 = make_float2(0.f, 0.f);
+        for (int i = 0; i < n; ++i) {
+          const float4 r2 = *reinterpret_cast<const float4*>(&sRY[i * TL_PT + 2 * pp]);
+          const float2 a = sA[i * TL_AS + c];
+          cfma_conj(g0, a, make_float2(r2.x, r2.y));
+          cfma_conj(g1, a, make_float2(r2.z, r2.w));
+        }
+        sG[(2 * pp) * TL_CT + c] = g0;
+        sG[(2 * pp + 1) * TL_CT + c] = g1;
+      }
+      __syncthreads();
+      if (2 * pg < count) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[q][j] = sG[(2 * pg + q) * TL_CT + cg + 16 * j];
+      }
+      __syncthreads();
     } else if (2 * pg < count)  // pixel pairs past the tile's count (few-RHS RBPG rounds) skip the GEMM
     for (int i = 0; i < n; ++i) {
       const float4 r2 = *reinterpret_cast<const float4*>(&sRY[i * TL_PT + 2 * pg]);
