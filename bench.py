@@ -136,13 +136,14 @@ def fp32_peak():
 
 def ncu_traffic(key: str):
     """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
-    (profiles/ncu_traffic.json, keyed workload/backend/pixels), or None when not captured."""
+    (profiles/ncu_traffic.json, keyed workload/backend/pixels) and the binding resource ncu
+    measured there, or Nones when not captured."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             e = json.load(fh)[key]
-        return float(e["dram_bytes_per_launch"]), e["source"]
+        return float(e["dram_bytes_per_launch"]), e["source"], e.get("binding")
     except Exception:
-        return None, None
+        return None, None, None
 
 
 def measure_cpu(batch, backend, k_max, cores, gpu_mean_iters, cfg_id, sample=None, hoist=False, min_wall=8.0, setup=None):
@@ -385,7 +386,7 @@ def run_b200(args):
     st = est.solution.status.cpu().numpy()
     its = est.solution.iterations.cpu().numpy()
 
-    traffic, traffic_src = ncu_traffic(f"cfg{args.config}/{args.backend}/{P_total}")
+    traffic, traffic_src, binding = ncu_traffic(f"cfg{args.config}/{args.backend}/{P_total}")
     line = None
     if rank == 0:
         line = {
@@ -411,6 +412,8 @@ def run_b200(args):
             "clocks": clk,
             "solver_stats": {"mean_iterations": float(its.mean()), "converged_frac": float((st == 0).mean()), "max_iters_frac": float((st == 1).mean())},
         }
+        if binding:  # the resource ncu saw saturating in this kernel (FP32 is not it)
+            line["roofline"]["binding"] = binding
         if not args.no_cpu_baseline and world == 1:
             cores = os.cpu_count() or 1
             mean_its = float(its.mean())

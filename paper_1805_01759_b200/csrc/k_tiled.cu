@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
           const double2 v = make_double2(fma(-alpha, 2.0 * (double)acc[q][j].x, y.x), fma(-alpha, 2.0 * (double)acc[q][j].y, y.y));
           const double mag2 = fma(v.x, v.x, v.y * v.y);
           double2 z = make_double2(0.0, 0.0);
-          if (mag2 > tau * tau) {
+          if (!(mag2 <= tau * tau)) {  // zero iff |v| <= tau; NaN propagates (prox.py:82-96)
             const double mag = sqrt(mag2);
             const double sc = 1.0 - tau / mag;
             z = make_double2(v.x * sc, v.y * sc);

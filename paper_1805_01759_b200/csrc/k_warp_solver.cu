@@ -399,7 +399,9 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           const double2 v = make_double2(fma(-alpha, (double)g[t].x, yv.x), fma(-alpha, (double)g[t].y, yv.y));
           const double mag2 = fma(v.x, v.x, v.y * v.y);
           double2 zz = make_double2(0.0, 0.0);
-          if (act && mag2 > tau2) {  // soft_threshold: zero iff |v| <= tau (prox.py:82-96)
+          // soft_threshold: zero iff |v| <= tau (prox.py:82-96); a NaN v stays NaN, as the
+          // reference's v * max(0, 1 - tau / max(|v|, tiny)) propagates it
+          if (act && !(mag2 <= tau2)) {
             // scale 1 - tau/|v| and |z| = |v| - tau from one fp64 reciprocal square root
 #if TB_WS_RSQRT
             const double rs = rsqrt(mag2);

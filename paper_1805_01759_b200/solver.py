@@ -14,6 +14,7 @@ streams.  There is no CPU fallback: without the library or a GPU these functions
 from __future__ import annotations
 
 import ctypes
+import os
 import hashlib
 import json
 import time
@@ -251,13 +252,14 @@ class Dictionary:
             _lib.check(lib.tb_ctx_create(dev.index, _lib.ptr(at), self.n, self.m, ctypes.byref(h)))
         self._h = h
         self._lib = lib
+        self._pid = os.getpid()  # a forked child (e.g. a CPU process pool) must not touch the context
         self._lip_full = None
         self._partitions = {}
         self._active_j = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and getattr(self, "_pid", None) == os.getpid():
             try:
                 self._lib.tb_ctx_destroy(h)
             except Exception:

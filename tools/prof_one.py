@@ -13,6 +13,6 @@ px = torch.from_numpy(batch.pixels).cuda()
 lam = d.default_lambda(px, 0.1)
 seeds = d.derive_seeds(2018, P)
 cfg = tb.SolverConfig(max_iters=500, tol=1e-6, num_blocks=8, seed=2018)
-r = d.solve(px, lam, cfg, be, seeds=seeds, precision=prec)
+r = d.solve(px, lam, cfg, be, seeds=seeds)
 torch.cuda.synchronize()
 print("mean iters", r.iterations.double().mean().item())
