@@ -95,6 +95,16 @@ int tb_default_lambda(tb_ctx* ctx, const void* pixels_dev, int64_t num_pixels, d
 int tb_derive_seeds(uint64_t run_seed, int64_t first_pixel_id, int64_t num_pixels,
                     uint64_t* seeds_dev, void* stream);
 
+/* Monte-Carlo realizations of simulate.py:297-335 on the device (synthesize_pixel, simulate.py:194-205,
+ * for the harness's two unit-amplitude scatterers snapped to grid columns col0/col1):
+ * pixels[r] = A[:, col0[r]] + e^{j phase[r]} A[:, col1[r]] + sqrt(sigma[r]^2 / 2) (N + jN), complex64 [count][n],
+ * phase NaN = drawn uniform(0, 2 pi); seeds[r] = the nested RBPG seed.  Draws come from Philox4x64-10
+ * keyed (seed, stream_ids[r]) (rng.py:17-24) with Box-Muller normals: statistically, not bit-,
+ * equivalent to the reference's numpy ziggurat draws.  Device arrays. */
+int tb_synthesize_pairs(tb_ctx* ctx, uint64_t seed, const uint64_t* stream_ids_dev, const int32_t* col0_dev,
+                        const int32_t* col1_dev, const float* phase_dev, const float* sigma_dev, int64_t count,
+                        void* pixels_dev, uint64_t* seeds_dev, void* stream);
+
 /* rbpg_solve / fista_solve / ista_solve (solver.py:250-390) over a pixel batch.
  *  pixels_dev  complex64 [P, n];  lambda_dev double [P];  seeds_dev uint64 [P] (RBPG only,
  *  may be NULL otherwise);  x_dev complex64 [P, m] out (Solution.x_hat);

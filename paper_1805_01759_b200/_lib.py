@@ -47,6 +47,7 @@ SIGNATURES = {
     "tb_set_lipschitz": (c_int32, [c_void_p, c_double]),
     "tb_default_lambda": (c_int32, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p]),
     "tb_derive_seeds": (c_int32, [c_uint64, c_int64, c_int64, c_void_p, c_void_p]),
+    "tb_synthesize_pairs": (c_int32, [c_void_p, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "tb_solve": (c_int32, [c_void_p, c_int32, ctypes.POINTER(SolverConfigC), c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "tb_tiled_create": (c_int32, [c_void_p, c_int32, ctypes.POINTER(SolverConfigC), c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),
     "tb_tiled_round_a": (c_int32, [c_void_p, c_void_p]),

@@ -130,6 +130,68 @@ cudaError_t launch_derive_seeds(uint64_t run_seed, long long first, long long P,
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ two-scatterer realizations
+// The Monte-Carlo realization of simulate.py:297-335 drawn on the device: g = A[:, c0] + e^{j phi}
+// A[:, c1] + sqrt(sigma^2 / 2) (N + jN) with unit amplitudes on grid columns c0, c1 (the reference
+// snaps both scatterers to the grid, simulate.py:312-322), one warp per realization, lane = row.
+// Every realization draws from Philox4x64-10 keyed (seed, stream_id) -- the reference's substream
+// (rng.py:17-24) -- in a fixed layout: raw 0 = the phase (numpy's next_double, used when phase is
+// NaN), raws 1 + 2i, 2 + 2i = the two uniforms Box-Muller turns into row i's complex normal, raw
+// 1 + 2n onwards = the nested RBPG seed (integers(0, 2^63 - 1), Lemire, as derive_seed).  The
+// normals are NOT numpy's ziggurat draws, so realizations are statistically (not bit-) equivalent
+// to the reference's.
+__global__ void synth_pair_kernel(const float2* __restrict__ A, int n, int m, uint64_t seed, const uint64_t* stream_ids,
+                                  const int* c0, const int* c1, const float* phase, const float* sigma, long long count,
+                                  float2* pixels, uint64_t* seeds) {
+  const int lane = threadIdx.x & 31;
+  const long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= count) return;
+  const uint64_t sid = stream_ids[r];
+  auto raw_at = [&](uint64_t k) {  // raw draw k of Philox(key=[seed, sid]): counter k/4 + 1, lane k % 4
+    uint64_t c[4] = {k / 4 + 1, 0ull, 0ull, 0ull};
+    philox4x64_10(c, seed, sid);
+    const int w = (int)(k & 3ull);
+    return w == 0 ? c[0] : w == 1 ? c[1] : w == 2 ? c[2] : c[3];
+  };
+  double ph = (double)phase[r];
+  if (ph != ph) ph = 2.0 * 3.141592653589793 * raw_to_unit(raw_at(0));  // uniform(0, 2 pi)
+  double sp, cp;
+  sincos(ph, &sp, &cp);
+  const double s = (double)sigma[r] * 0.7071067811865476;
+  for (int i = lane; i < n; i += 32) {
+    const float2 a = A[(size_t)i * m + c0[r]], b = A[(size_t)i * m + c1[r]];
+    double gx = (double)a.x + cp * b.x - sp * b.y, gy = (double)a.y + cp * b.y + sp * b.x;
+    if (s > 0.0) {
+      const double u1 = raw_to_unit(raw_at(1 + 2 * (uint64_t)i)), u2 = raw_to_unit(raw_at(2 + 2 * (uint64_t)i));
+      const double rad = sqrt(-2.0 * log1p(-u1));  // 1 - u1 in (0, 1]
+      double sn, cn;
+      sincospi(2.0 * u2, &sn, &cn);
+      gx = fma(s, rad * cn, gx);
+      gy = fma(s, rad * sn, gy);
+    }
+    pixels[(size_t)r * n + i] = make_float2((float)gx, (float)gy);
+  }
+  if (lane == 0) {
+    const uint64_t rng_excl = 0x7FFFFFFFFFFFFFFFull;
+    for (uint64_t k = 1 + 2 * (uint64_t)n;; ++k) {
+      const uint64_t raw = raw_at(k);
+      if (raw * rng_excl >= 2ull) {
+        seeds[r] = __umul64hi(raw, rng_excl);
+        break;
+      }
+    }
+  }
+}
+
+cudaError_t launch_synth_pair(const float2* A, int n, int m, uint64_t seed, const uint64_t* stream_ids, const int* c0,
+                              const int* c1, const float* phase, const float* sigma, long long count, float2* pixels,
+                              uint64_t* seeds, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  count_launch();
+  synth_pair_kernel<<<(unsigned)((count + 7) / 8), 256, 0, st>>>(A, n, m, seed, stream_ids, c0, c1, phase, sigma, count, pixels, seeds);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ power iteration
 // Single-CTA-per-range variant: the whole iteration loop runs on device.
 // v: complex128 work vectors, one per range, concatenated (initialised with the start vectors).

@@ -10,6 +10,9 @@ namespace tb {
 cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B, long long P, double beta,
                                   double* lam, int num_sms, cudaStream_t st);
 cudaError_t launch_derive_seeds(uint64_t run_seed, long long first, long long P, uint64_t* seeds, cudaStream_t st);
+cudaError_t launch_synth_pair(const float2* A, int n, int m, uint64_t seed, const uint64_t* stream_ids, const int* c0,
+                              const int* c1, const float* phase, const float* sigma, long long count, float2* pixels,
+                              uint64_t* seeds, cudaStream_t st);
 cudaError_t launch_power_small(const float2* A, int n, int m, const long long* starts, const long long* stops,
                                int num_ranges, double2* v, double2* uscratch, int max_iter, double rtol,
                                double* out_dev, cudaStream_t st);

@@ -319,6 +319,16 @@ int tb_default_lambda(tb_ctx* c, const void* pixels, int64_t P, double beta, dou
   return TB_OK;
 }
 
+int tb_synthesize_pairs(tb_ctx* c, uint64_t seed, const uint64_t* stream_ids, const int32_t* col0, const int32_t* col1,
+                        const float* phase, const float* sigma, int64_t count, void* pixels, uint64_t* seeds, void* stream) {
+  if (!c || count < 0 || (count > 0 && (!stream_ids || !col0 || !col1 || !phase || !sigma || !pixels || !seeds)))
+    return fail(TB_ERR_INVALID, "invalid synthesis arguments");
+  TB_CUDA(cudaSetDevice(c->device));
+  TB_CUDA(tb::launch_synth_pair(c->A, (int)c->n, (int)c->m, seed, stream_ids, col0, col1, phase, sigma, count, (float2*)pixels, seeds,
+                                (cudaStream_t)stream));
+  return TB_OK;
+}
+
 int tb_derive_seeds(uint64_t run_seed, int64_t first, int64_t P, uint64_t* seeds, void* stream) {
   if (P < 0 || (P > 0 && !seeds)) return fail(TB_ERR_INVALID, "invalid seeds arguments");
   TB_CUDA(tb::launch_derive_seeds(run_seed, first, P, seeds, (cudaStream_t)stream));

@@ -13,7 +13,9 @@ realizations themselves are drawn on the host exactly as the reference draws the
 substream keyed (scenario seed, cell * realizations + r); phase, ziggurat normals, nested solver
 seed in the same order), so the synthesized pixels are bit-identical to the reference's and the
 per-realization outcomes differ only where the float32 solve lands on the other side of a
-detection decision.
+detection decision.  ``draws="device"`` instead draws the realizations on the GPU
+(``tb_synthesize_pairs``: the same Philox substreams, Box-Muller normals), so the whole sweep runs
+on the device with statistically equivalent draws.
 """
 
 from __future__ import annotations
@@ -228,9 +230,13 @@ def _draw_all(base, grid, setup, items, workers: int):
 
 
 def monte_carlo_outcomes(base: Scenario, kappas, snrs, methods, realizations: int, setup: MonteCarloSetup | None = None,
-                         workers: int = 1, device=None):
+                         workers: int = 1, device=None, draws: str = "host"):
     """Per-realization detection outcomes, cells in the reference's (kappa, snr, method) order.
 
+    ``draws`` "host": every realization drawn on the host exactly as the reference draws it
+    (bit-identical pixels and nested seeds).  "device": drawn by the synthesis kernel
+    (``Dictionary.synthesize_pairs``) from the same Philox substreams with Box-Muller normals --
+    statistically equivalent, and the whole harness then runs on the GPU.
     Returns (cells, outcomes) with outcomes a bool array [len(cells), realizations].
     """
     from .slimmer import PipelineConfig, pipeline_batch
@@ -245,13 +251,28 @@ def monte_carlo_outcomes(base: Scenario, kappas, snrs, methods, realizations: in
     grid = harness_grid(base, setup)
     unit = separation_unit(base.geometry)
     tol = setup.tol_factor * unit
+    if draws not in ("host", "device"):
+        raise ConfigurationError(f"draws must be 'host' or 'device', got {draws!r}")
     cells = [(k, s, meth) for k in kappas for s in snrs for meth in methods]
     items = [(cells[c][0], cells[c][1], c * realizations + r) for c in range(len(cells)) for r in range(realizations)]
-    drawn = _draw_all(base, grid, setup, items, workers)
-    pixels = np.stack([d[0] for d in drawn]).astype(np.complex64)
-    seeds = np.array([d[1] for d in drawn], dtype=np.uint64)
-    truths = [d[2] for d in drawn]
     d = Dictionary(steering_dictionary(base.geometry, grid, device=device))
+    if draws == "host":
+        drawn = _draw_all(base, grid, setup, items, workers)
+        pixels = np.stack([d_[0] for d_ in drawn]).astype(np.complex64)
+        seeds = np.array([d_[1] for d_ in drawn], dtype=np.uint64)
+        truths = [d_[2] for d_ in drawn]
+    else:
+        # the two scatterers at the grid points nearest -/+ kappa unit / 2, unit amplitude, phases 0
+        # and delta_phi (drawn when None), noise variance from the first scatterer (simulate.py:309-329)
+        elev = np.asarray(grid.elevation, dtype=float)
+        unit_half = np.array([it[0] for it in items]) * unit / 2.0
+        c0 = np.abs(elev[None, :] + unit_half[:, None]).argmin(axis=1)
+        c1 = np.abs(elev[None, :] - unit_half[:, None]).argmin(axis=1)
+        phase = np.full(len(items), np.nan if setup.delta_phi is None else setup.delta_phi, dtype=np.float32)
+        sigma = np.sqrt(10.0 ** (-np.array([it[1] for it in items]) / 10.0)).astype(np.float32)
+        pixels, seeds = d.synthesize_pairs(base.seed, [it[2] for it in items], c0, c1, phase, sigma)
+        seeds = seeds.view(torch_int64())  # CUDA gathers do not take uint64; solve() reinterprets int64 seeds
+        truths = [[float(elev[a]), float(elev[b])] for a, b in zip(c0, c1)]
     outcomes = np.zeros(len(items), dtype=bool)
     for meth in dict.fromkeys(methods):
         rows = np.array([i for i in range(len(items)) if cells[i // realizations][2] == meth])
@@ -260,7 +281,8 @@ def monte_carlo_outcomes(base: Scenario, kappas, snrs, methods, realizations: in
         for mu in np.unique(mus):
             grp = rows[mus == mu]
             cfg = PipelineConfig(solver=setup.solver, backend=meth, k_max=setup.k_max, wiener_mu=float(mu))
-            est = pipeline_batch(d, pixels[grp], grid, cfg, seeds=seeds[grp] if meth == "rbpg" else None)
+            sel = grp if draws == "host" else _torch_index(grp, pixels.device)
+            est = pipeline_batch(d, pixels[sel], grid, cfg, seeds=seeds[sel] if meth == "rbpg" else None)
             order = est.model_order.cpu().numpy()
             elev = est.elevations.cpu().numpy()
             err = est.error.cpu().numpy()
@@ -270,10 +292,22 @@ def monte_carlo_outcomes(base: Scenario, kappas, snrs, methods, realizations: in
     return cells, outcomes.reshape(len(cells), realizations)
 
 
+def torch_int64():
+    import torch
+
+    return torch.int64
+
+
+def _torch_index(rows, device):
+    import torch
+
+    return torch.as_tensor(np.asarray(rows, dtype=np.int64), device=device)
+
+
 def monte_carlo_detection(base: Scenario, kappas, snrs, methods, realizations: int, setup: MonteCarloSetup | None = None,
-                          workers: int = 1, device=None) -> list:
+                          workers: int = 1, device=None, draws: str = "host") -> list:
     """Detection rate per (kappa, SNR, method) cell with Wilson 95% CIs (simulate.py:354-424)."""
-    cells, outcomes = monte_carlo_outcomes(base, kappas, snrs, methods, realizations, setup, workers, device)
+    cells, outcomes = monte_carlo_outcomes(base, kappas, snrs, methods, realizations, setup, workers, device, draws)
     out = []
     for (kappa, snr, meth), hits in zip(cells, outcomes):
         h = int(hits.sum())

@@ -337,6 +337,31 @@ class Dictionary:
             _lib.check(self._lib.tb_derive_seeds(int(run_seed) & (2**64 - 1), int(first_pixel_id), int(num_pixels), _lib.ptr(seeds), self._stream()))
         return seeds
 
+    def synthesize_pairs(self, seed: int, stream_ids, col0, col1, phase, sigma):
+        """Two-scatterer Monte-Carlo realizations on the device (tb_synthesize_pairs; simulate.py:297-335):
+        pixels[r] = A[:, col0[r]] + e^{j phase[r]} A[:, col1[r]] + complex normal noise of variance sigma[r]^2
+        (phase NaN = drawn), plus each realization's nested RBPG seed.  Statistically equivalent to
+        the reference's draws (Philox substreams, Box-Muller normals).  Returns (pixels c64 [R, n],
+        seeds u64 [R]) on this device."""
+        torch = _torch()
+        dev = self.device
+        sid = torch.as_tensor(np.asarray(stream_ids, dtype=np.uint64).astype(np.int64)).to(dev).view(torch.uint64)
+        c0 = torch.as_tensor(np.asarray(col0, dtype=np.int32)).to(dev)
+        c1 = torch.as_tensor(np.asarray(col1, dtype=np.int32)).to(dev)
+        ph = torch.as_tensor(np.asarray(phase, dtype=np.float32)).to(dev)
+        sg = torch.as_tensor(np.asarray(sigma, dtype=np.float32)).to(dev)
+        r = int(sid.numel())
+        if not (c0.numel() == c1.numel() == ph.numel() == sg.numel() == r):
+            raise ConfigurationError("one column pair, phase and sigma per realization")
+        if r and (int(min(c0.min(), c1.min())) < 0 or int(max(c0.max(), c1.max())) >= self.m):
+            raise ConfigurationError("scatterer columns outside the dictionary")
+        pix = torch.empty((r, self.n), dtype=torch.complex64, device=dev)
+        seeds = torch.empty(r, dtype=torch.uint64, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(self._lib.tb_synthesize_pairs(self._h, int(seed) & (2**64 - 1), _lib.ptr(sid), _lib.ptr(c0), _lib.ptr(c1),
+                                                     _lib.ptr(ph), _lib.ptr(sg), r, _lib.ptr(pix), _lib.ptr(seeds), self._stream()))
+        return pix, seeds
+
     def solve(self, pixels, lam, config: SolverConfig, backend: str = "rbpg", seeds=None, history: bool = False, out=None, path: str = "auto", allreduce=None) -> BatchSolution:
         """Solve every pixel of a stack on the device.
 

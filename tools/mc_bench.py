@@ -52,5 +52,13 @@ res = S.monte_carlo_detection(base, KAPPAS, SNRS, METHODS, R, setup, workers=W)
 torch.cuda.synchronize()
 dt = time.time() - t0
 n = len(items)
-print(json.dumps({"impl": "b200", "realizations": n, "seconds": dt, "realizations_per_s": n / dt, "host_synthesis_s": t_host,
+print(json.dumps({"impl": "b200", "draws": "host", "realizations": n, "seconds": dt, "realizations_per_s": n / dt, "host_synthesis_s": t_host,
                   "workers": W, "p_d": {f"{r.kappa}/{r.snr_db}/{r.method}": r.p_d for r in res}}))
+S.monte_carlo_detection(base, KAPPAS, SNRS, METHODS, 8, setup, draws="device")  # warm-up
+torch.cuda.synchronize()
+t0 = time.time()
+res2 = S.monte_carlo_detection(base, KAPPAS, SNRS, METHODS, R, setup, draws="device")
+torch.cuda.synchronize()
+dt2 = time.time() - t0
+print(json.dumps({"impl": "b200", "draws": "device", "realizations": n, "seconds": dt2, "realizations_per_s": n / dt2,
+                  "p_d": {f"{r.kappa}/{r.snr_db}/{r.method}": r.p_d for r in res2}}))
