@@ -268,7 +268,9 @@ def test_rbpg_block_counts_vs_oracle(tb, num_blocks):
 def test_full_size_cfg2_sampled_vs_oracle(tb):
     """The BASELINE cfg2 batch at full size (1,048,576 pixels, RBPG, the bench's settings): 192
     pixels sampled across the whole batch (including the last ones, whose seeds come from large
-    pixel ids) match the oracle exactly in iterations, status and support, objective within 1e-6."""
+    pixel ids) match the oracle exactly in iterations, status and support, objective within 1e-6.
+    Nothing is handed from the GPU to the oracle: it computes its own lambda (prox.py:153-161) and,
+    as the reference does, its own block partition on every solve (solver.py:267)."""
     from paper_1805_01759_b200.synth import make_config
 
     batch = make_config(2)
@@ -278,12 +280,13 @@ def test_full_size_cfg2_sampled_vs_oracle(tb):
     rng = np.random.default_rng(7)
     idx = np.sort(np.concatenate([rng.choice(batch.num_pixels, 184, replace=False), np.arange(batch.num_pixels - 8, batch.num_pixels)]))
     idx = np.unique(idx)
-    lam = est.lam.cpu().numpy()[idx]
+    a64 = batch.dictionary.astype(np.complex128)
+    lam = np.array([O.default_lambda(a64, batch.pixels[p].astype(np.complex128), 0.1) for p in idx])
+    np.testing.assert_allclose(est.lam.cpu().numpy()[idx], lam, rtol=1e-13)
     seeds = np.array([O.derive_seed(2018, int(p)) for p in idx], dtype=np.uint64)
     grid = OB.GridDesc(batch.grid.elevation, batch.grid.motion_axes)
-    lips = d.partition(8).lipschitz
-    ref = OB.run(batch.dictionary.astype(np.complex128), batch.pixels[idx], lam, "rbpg", seeds=seeds, grid=grid, k_max=batch.k_max,
-                 lips=lips, max_iters=500, tol=1e-6, num_blocks=8)
+    ref = OB.run(a64, batch.pixels[idx], lam, "rbpg", seeds=seeds, grid=grid, k_max=batch.k_max,
+                 lips=None, max_iters=500, tol=1e-6, num_blocks=8)
     its = est.solution.iterations.cpu().numpy()[idx]
     st = est.solution.status.cpu().numpy()[idx]
     ff = est.solution.objective_final.cpu().numpy()[idx]
