@@ -258,11 +258,20 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       // entirely past the range are skipped with a warp-uniform test.
       // DC: the block's d_b is loaded from L2 here and first used in the backtracking loop, so the
       // load latency hides behind the adjoint.
-      double2 dvb[DC ? MAXT : 1];
+      // XR: the block's x_b also stays in registers for the whole iteration (one shared read instead
+      // of one per trial plus one in the update; measured +1.5% on cfg2, but -19% on cfg3 where A is
+      // read through L1 and -4% on the latency-bound small batches, so only for a full SM with A in
+      // shared memory)
+      constexpr bool XR = DC && ASMEM && !SHFL;
+      double2 dvb[DC ? MAXT : 1], xr[XR ? MAXT : 1];
 #pragma unroll
       for (int t = 0; t < (DC ? MAXT : 1); ++t) {
         dvb[t] = make_double2(0.0, 0.0);
-        if (DC && (t == 0 || 32 * t < width)) dvb[t] = dg[cs + min(lane + 32 * t, width - 1)];
+        if (XR) xr[XR ? t : 0] = make_double2(0.0, 0.0);
+        if (DC && (t == 0 || 32 * t < width)) {
+          dvb[t] = dg[cs + min(lane + 32 * t, width - 1)];
+          if (XR) xr[XR ? t : 0] = xs[cs + min(lane + 32 * t, width - 1)];
+        }
       }
 #pragma unroll
       for (int t = 0; t < (DC ? 0 : MAXT); ++t) {
@@ -385,8 +394,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           const int cl = lane + 32 * t;
           const bool act = cl < width;
           const int col = cs + (act ? cl : 0);
-          // y = x + m_k d recomputed from shared memory (keeps registers for occupancy)
-          const double2 xv = xs[col];
+          // y = x + m_k d; FISTA/ISTA recompute it from shared memory (keeps registers for occupancy)
+          const double2 xv = XR ? xr[XR ? t : 0] : xs[col];
           double2 yv = xv;
           if (DC) {
             yv.x = fma(mk, dvb[t].x, xv.x);
@@ -499,7 +508,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           const int cl = lane + 32 * t;
           if (cl < width) {
             // accept: prev_b <- x_b, x_b <- z_b; reject: prev_b <- x_b (solver.py:318-325)
-            const double2 xv = xs[cs + cl], zv = accept ? z[RB ? t : 0] : xv;
+            const double2 xv = XR ? xr[XR ? t : 0] : xs[cs + cl], zv = accept ? z[RB ? t : 0] : xv;
             if (DC)
               dg[cs + cl] = make_double2(zv.x - xv.x, zv.y - xv.y);
             else
