@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libtomobpdn_b200.so")
-SOURCES = ["tb_api.cu", "k_warp_solver.cu", "k_setup.cu", "k_select.cu", "k_tiled.cu", "k_tc_tiled.cu"]
+SOURCES = ["tb_api.cu", "k_warp_solver.cu", "k_fista_tile.cu", "k_setup.cu", "k_select.cu", "k_tiled.cu", "k_tc_tiled.cu"]
+OBJDIR = os.path.join(LIBDIR, "obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -39,8 +40,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     from concurrent.futures import ThreadPoolExecutor
 
+    # objects are kept (git-ignored) so that a change to one source recompiles that source only;
+    # a change to any header recompiles everything
+    os.makedirs(OBJDIR, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")]
+    headers.append(os.path.join(HERE, "..", "include", "tomobpdn_b200.h"))
+    hdr_time = max(os.path.getmtime(h) for h in headers if os.path.exists(h))
+
     def compile_one(src):
-        obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
+        obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_time, os.path.getmtime(os.path.join(CSRC, src))):
+            return obj
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
@@ -52,8 +62,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs], check=True)
     os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
     return LIB
 
 

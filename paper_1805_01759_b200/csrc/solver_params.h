@@ -67,5 +67,9 @@ __host__ __device__ inline size_t block_table_bytes(int J) {
 }
 
 cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps);
+// Team-tiled FISTA/ISTA kernel (k_fista_tile.cu): the dictionary must fit in shared memory beside
+// >= 8 pixel slots; m <= 512 (the extrapolation memory and the candidate live in tensor memory).
+bool fista_tile_fits(int n, int m);
+cudaError_t launch_fista_tile(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps);
 
 }  // namespace tb

@@ -825,6 +825,10 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   S.status = status;
   S.queue = c->queue;
   S.mk = c->mk;
+  // ISTA/FISTA with the dictionary in shared memory run the team-tiled kernel (TB_FISTA_KERNEL=warp
+  // selects the warp-per-pixel kernel: A/B and bit-identity tests)
+  const char* fk = getenv("TB_FISTA_KERNEL");
+  const bool tile = solver != TB_SOLVER_RBPG && tb::fista_tile_fits((int)c->n, (int)c->m) && !(fk && strcmp(fk, "warp") == 0);
   if (solver == TB_SOLVER_RBPG && TB_WS_DCACHE) {
     const size_t need = (size_t)c->num_sms * 32 * (size_t)c->m;  // >= resident warp slots x m
     if (c->dglob_elems < need) {
@@ -841,7 +845,10 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   TB_CUDA(ctx_acquire(c, st));
   TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
   int warps = 0;
-  TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
+  if (tile)
+    TB_CUDA(tb::launch_fista_tile(S, c->num_sms, st, &warps));
+  else
+    TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
   TB_CUDA(ctx_release(c, st));
   return TB_OK;
 }
