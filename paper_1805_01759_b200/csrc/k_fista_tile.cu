@@ -1,36 +1,40 @@
-// Team-tiled FISTA / ISTA solver for dictionaries that fit in shared memory (cfg1, cfg2).
+// ISTA / FISTA solver with the per-pixel iterate state in TENSOR MEMORY (cfg1-3 shapes: m <= 512).
 //
 // Reference semantics (paths relative to /root/reference/pkg/src/tomobpdn):
 //   _full_vector_pg solver.py:341-376   (ISTA/FISTA, per-iteration backtracking from alpha0)
 //   soft_threshold  prox.py:82-96, line_search_ok prox.py:107-119, _window_converged solver.py:227-231
 //
-// FISTA's gradient g = 2 A^H (A y - b) uses every column of the shared dictionary for every pixel,
-// so over a pixel batch it is a dense contraction G = A^H R_y.  The warp-per-pixel kernel
-// (k_warp_solver.cu) evaluates it as one matrix-vector product per warp and fetches every A element
-// from shared memory once per pixel and iteration: its shared-memory pipe saturates at 31% of the
-// FP32 peak (cfg2).  Here a TEAM of 4 warps owns 4 pixel slots and iterates them in lock step:
-//   R  each warp (lane = row) forms its pixel's residual r_y = A y - b           -> shared memory
-//   G  the team's 128 threads compute G[:, 4 pixels] with CT columns x 4 pixels register tiles:
-//      one A element load feeds 4 pixels, one r_y broadcast feeds CT columns, packed FFMA2
-//   P  each warp runs its pixel's backtracking (fp64 prox, sparse fp64 forward product A z),
-//      update, objective and window stop; a finished pixel is written out and the slot refilled
-//      from the global atomic queue.
-// Teams synchronise with their own named barrier (bar.sync id, 128) only; the 4 teams of a CTA
-// share the dictionary in shared memory and drift out of phase, so one team's FP32 contraction
-// overlaps another's fp64 prox / shared-memory work.
+// The warp-per-pixel kernel (k_warp_solver.cu) keeps x, d = x - prev and the candidate z of a pixel
+// in shared memory: 17.4 KB per pixel on cfg2, so only 9 warps are resident beside the 60 KB
+// dictionary and the SM idles on latency (IPC 1.6).  Here one warp still owns one pixel, but
+//   * d and z live in tensor memory, used as a lane-private scratchpad: warp w owns TMEM lanes
+//     32 (w % 4) .. + 31 and columns 128 (w / 4) .. + 127, lane l keeps its columns l + 32 t as
+//     double2 at TMEM columns 4 t (d) and 4 (T + t) (z), T = ceil(m / 32); tcgen05.ld / tcgen05.st
+//     (LDTM / STTM) have a ~12-cycle latency and do not use the shared-memory data pipe;
+//   * the nonzero entries of z are compacted for the sparse forward product into a 64-entry buffer
+//     that is flushed every two column passes (same ascending column order);
+//   * per-lane bit masks record where x and d are nonzero (no zero-fill at pixel start);
+//   * the column passes of prox and update are rolled loops of 2-pass straight-line chunks (fully
+//     unrolled, 16 warps at different places of ~250 KB of code thrashed the instruction cache).
+// A slot is 10 KB on cfg2: 16 warps per SM, IPC 2.4, cfg2 FISTA 108 -> 82 ms per 65,536 pixels.
 //
-// Results are bit-identical to the warp kernel: every output element sees the same sequence of
-// roundings (rows summed in order with the same two packed FFMA2 per row; the fp64 forward product
-// visits the nonzero columns in ascending order; the same butterfly reductions).
-// Sparsity shortcuts that cannot change a result: the extrapolation memory d = x - prev lives in
-// global memory (L2) and only its nonzero entries are ever stored or loaded (per-lane bit masks for
-// x != 0 and d != 0); a pass of 32 columns with y = 0 and |g|^2 <= lambda^2 (1 - 1e-5) in fp32 is
-// skipped, because its exact fp64 prox would return 0 for every lane.
+// TEAM = true is the 4-warp-team variant asked for by the round-1 review ("CTA-tiled dense
+// contraction"): a team iterates its 4 pixels in lock step and computes G = A^H R_y[:, 4 pixels]
+// with CT columns x 4 pixels register tiles (one A load feeds 4 pixels: shared wavefronts 994 -> 758
+// per pixel-iteration), synchronising on its own named barrier.  It is bit-identical but SLOWER
+// (110 vs 82 ms): the contraction is only 43% of the instructions, the team barrier waits for the
+// slowest of 4 prox phases (20% of the stall samples), and a warp executes as many instructions as
+// before.  Kept selectable (TB_FISTA_KERNEL=team) with its identity test.
+//
+// Results are bit-identical to the warp kernel in both modes: every output element sees the same
+// sequence of roundings (rows summed in order with the same two packed FFMA2 per row; the fp64
+// forward product visits the nonzero columns in ascending order; the same butterfly reductions).
 #include <float.h>
 #include <stdlib.h>
 
 #include "common.cuh"
 #include "solver_params.h"
+#include "warp_adjoint.cuh"
 
 namespace tb {
 
@@ -75,7 +79,15 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ double2 tmem_val(const uint32_t (&r)[4]) { return make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2])); }
 
-template <int CT, int MAXQ>
+// ASMEM: the dictionary is staged in shared memory (cfg1, cfg2).  Otherwise (cfg3: 200 KiB) it is
+// read from global memory: in the contraction each thread streams its own CT columns (coalesced,
+// one load per element per TEAM iteration instead of per pixel iteration), the sparse forward
+// product gathers its columns through L1/L2.
+// TEAM = false ("solo"): no teams and no barriers -- every warp computes its own pixel's gradient
+// with the column-lane adjoint of the warp kernel (warp_adjoint.cuh), keeping this kernel's compact
+// slot (d and z in tensor memory, 64-entry compaction buffer: 16 resident warps instead of the warp
+// kernel's 9 on cfg2).
+template <int CT, int MAXQ, bool ASMEM, bool TEAM>
 __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -85,12 +97,14 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
   const bool ista = P.mode == SOLVER_ISTA;
 
   // ---- dictionary staged once per CTA, row-major with an odd row stride
-  float2* As = reinterpret_cast<float2*>(smem);
-  const size_t a_bytes = (((size_t)n * ms) * sizeof(float2) + 15) & ~(size_t)15;
-  for (int idx = threadIdx.x; idx < n * m; idx += blockDim.x) {
-    const int i = idx / m, c = idx - i * m;
-    As[(size_t)i * ms + c] = __ldg(&P.A[idx]);
-  }
+  const int as = ASMEM ? ms : m;  // row stride of the dictionary as the kernel reads it
+  const float2* As = ASMEM ? reinterpret_cast<const float2*>(smem) : P.A;
+  const size_t a_bytes = ASMEM ? (((size_t)n * ms) * sizeof(float2) + 15) & ~(size_t)15 : 0;
+  if (ASMEM)
+    for (int idx = threadIdx.x; idx < n * m; idx += blockDim.x) {
+      const int i = idx / m, c = idx - i * m;
+      reinterpret_cast<float2*>(smem)[(size_t)i * ms + c] = __ldg(&P.A[idx]);
+    }
   int* s_act = reinterpret_cast<int*>(smem + a_bytes);  // [warps] slot-active flags
   const size_t slot_bytes = fista_tile_slot_bytes(n, m);
   unsigned char* slots = smem + a_bytes + 64 * sizeof(int);
@@ -129,14 +143,14 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
   auto forward_accum = [&](int cnt, double2* acc) {
     const float2* arow[MAXQ];
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) arow[q] = As + (size_t)min(lane + 32 * q, n - 1) * ms;
+    for (int q = 0; q < MAXQ; ++q) arow[q] = As + (size_t)min(lane + 32 * q, n - 1) * as;
     int e = 0;
     for (; e + 2 <= cnt; e += 2) {
       const int2 cc = *reinterpret_cast<const int2*>(clist + e);
       const double2 v0 = zs[e], v1 = zs[e + 1];
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const float2 a0 = arow[q][cc.x], a1 = arow[q][cc.y];
+        const float2 a0 = ASMEM ? arow[q][cc.x] : __ldg(arow[q] + cc.x), a1 = ASMEM ? arow[q][cc.y] : __ldg(arow[q] + cc.y);
         acc[q].x = fma((double)a0.x, v0.x, fma(-(double)a0.y, v0.y, acc[q].x));
         acc[q].y = fma((double)a0.x, v0.y, fma((double)a0.y, v0.x, acc[q].y));
         acc[q].x = fma((double)a1.x, v1.x, fma(-(double)a1.y, v1.y, acc[q].x));
@@ -148,7 +162,7 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
       const double2 v = zs[e];
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const float2 a = arow[q][c];
+        const float2 a = ASMEM ? arow[q][c] : __ldg(arow[q] + c);
         acc[q].x = fma((double)a.x, v.x, fma(-(double)a.y, v.y, acc[q].x));
         acc[q].y = fma((double)a.x, v.y, fma((double)a.y, v.x, acc[q].y));
       }
@@ -215,6 +229,22 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
         }
       }
     }
+    if (!TEAM) {
+      if (!active) break;
+      __syncwarp();
+      // ---- gradient, one warp per pixel: lane = column, ceil(m / 32) passes, rows summed in order
+      constexpr int MAXT = 4 * CT;
+      float2 acc[MAXT];
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) acc[t] = make_float2(0.f, 0.f);
+      const int passes = (m + 31) >> 5;
+      adjoint_dispatch<1, MAXT, ASMEM, false>(passes, acc, As + lane, as, 32, ry4, n, lane + 32 * (passes - 1) < m);
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t)
+        if (lane + 32 * t < m) gs[lane + 32 * t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
+      __syncwarp();
+    }
+    if (TEAM) {
     if (lane == 0) s_act[warp] = active ? 1 : 0;
     team_bar(team + 1);
     {
@@ -240,11 +270,11 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
         ulonglong2 r[FT_TEAM];
 #pragma unroll
         for (int q = 0; q < FT_TEAM; ++q) r[q] = reinterpret_cast<const ulonglong2*>(rbase + (size_t)q * slot_bytes)[i];
-        const float2* arow = As + (size_t)i * ms;
+        const float2* arow = As + (size_t)i * as;
 #pragma unroll
         for (int j = 0; j < CT; ++j) {
           if (j * 128 + wt * 32 < m) {  // warp-uniform: this warp has columns in column set j
-            const float2 a = arow[cj[j]];
+            const float2 a = ASMEM ? arow[cj[j]] : __ldg(arow + cj[j]);
             const unsigned long long aa = pack2(a.x, a.x), bb = pack2(a.y, a.y);
 #pragma unroll
             for (int q = 0; q < FT_TEAM; ++q) {
@@ -268,6 +298,7 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
     }
     team_bar(team + 1);
     if (!active) continue;
+    }  // TEAM
 
     // ---- backtracking (solver.py:353-361; prox.py:122-150), prox step in fp64
     double2 ay[MAXQ];
@@ -481,13 +512,31 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_s));
 }
 
-bool fista_tile_fits(int n, int m) {
-  if (m > 512 || n > 128) return false;
+// Shared-memory plan: the dictionary beside >= 8 slots if it fits, else slots only (A from global)
+static bool fista_tile_plan(int n, int m, bool* asmem) {
+  if (m > 512 || n > 128) return false;  // 8 ceil(m / 32) tensor-memory columns per warp <= 128
+  const size_t cap = 227 * 1024 - 64, slot = fista_tile_slot_bytes(n, m);
   const size_t a_bytes = (((size_t)n * (m | 1)) * sizeof(float2) + 15) & ~(size_t)15;
-  return a_bytes + 64 * sizeof(int) + 2 * FT_TEAM * fista_tile_slot_bytes(n, m) <= 227 * 1024 - 64;
+  const char* ev = getenv("TB_FISTA_TILE_ASMEM");  // 0: force the global-memory dictionary (A/B)
+  const bool want = !(ev && atoi(ev) == 0);
+  *asmem = want && a_bytes + 64 * sizeof(int) + 2 * FT_TEAM * slot <= cap;
+  return *asmem || 64 * sizeof(int) + 2 * FT_TEAM * slot <= cap;
+}
+static int fista_tile_warps(int n, int m, bool asmem) {
+  const size_t slot = fista_tile_slot_bytes(n, m);
+  const size_t a_bytes = asmem ? (((size_t)n * (m | 1)) * sizeof(float2) + 15) & ~(size_t)15 : 0;
+  const int warps = (int)((227 * 1024 - 64 - a_bytes - 64 * sizeof(int)) / slot);
+  return warps > 16 ? 16 : warps / FT_TEAM * FT_TEAM;
+}
+bool fista_tile_fits(int n, int m, bool* asmem, int* slots) {
+  bool a = false;
+  const bool ok = fista_tile_plan(n, m, &a);
+  if (asmem) *asmem = a;
+  if (slots) *slots = ok ? fista_tile_warps(n, m, a) : 0;
+  return ok;
 }
 
-template <int CT>
+template <int CT, bool ASMEM, bool TEAM>
 static cudaError_t launch_ft_q(const SolveParams& P, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -497,20 +546,31 @@ static cudaError_t launch_ft_q(const SolveParams& P, int maxq, int warps, size_t
     return cudaGetLastError();
   };
   switch (maxq) {
-    case 1: return go(fista_tile_kernel<CT, 1>);
-    case 2: return go(fista_tile_kernel<CT, 2>);
-    case 4: return go(fista_tile_kernel<CT, 4>);
+    case 1: return go(fista_tile_kernel<CT, 1, ASMEM, TEAM>);
+    case 2: return go(fista_tile_kernel<CT, 2, ASMEM, TEAM>);
+    case 4: return go(fista_tile_kernel<CT, 4, ASMEM, TEAM>);
+    default: return cudaErrorInvalidValue;
+  }
+}
+template <bool ASMEM, bool TEAM>
+static cudaError_t launch_ft_ct(const SolveParams& P, int ct, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
+  switch (ct) {
+    case 1: return launch_ft_q<1, ASMEM, TEAM>(P, maxq, warps, smem, grid, st);
+    case 2: return launch_ft_q<2, ASMEM, TEAM>(P, maxq, warps, smem, grid, st);
+    case 3: return launch_ft_q<3, ASMEM, TEAM>(P, maxq, warps, smem, grid, st);
+    case 4: return launch_ft_q<4, ASMEM, TEAM>(P, maxq, warps, smem, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-// One CTA per SM, up to 16 pixel slots (4 teams) beside the dictionary; persistent, queue-fed.
-cudaError_t launch_fista_tile(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps) {
+// One CTA per SM, up to 16 pixel slots (4 teams); persistent, queue-fed.
+cudaError_t launch_fista_tile(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps, bool team) {
+  bool asmem = false;
+  if (!fista_tile_plan(P.n, P.m, &asmem)) return cudaErrorInvalidValue;
   const size_t slot = fista_tile_slot_bytes(P.n, P.m);
-  const size_t a_bytes = (((size_t)P.n * P.ms) * sizeof(float2) + 15) & ~(size_t)15;
-  const size_t cap = 227 * 1024 - 64, fixed = a_bytes + 64 * sizeof(int);  // 16 static bytes (TMEM base)
-  int warps = (int)((cap - fixed) / slot);
-  warps = warps > 16 ? 16 : warps / FT_TEAM * FT_TEAM;
+  const size_t a_bytes = asmem ? (((size_t)P.n * P.ms) * sizeof(float2) + 15) & ~(size_t)15 : 0;
+  const size_t fixed = a_bytes + 64 * sizeof(int);  // + 16 static bytes (TMEM base), inside the plan's margin
+  int warps = fista_tile_warps(P.n, P.m, asmem);
   if (const char* wc = getenv("TB_WARPS_CAP")) {  // tuning/diagnostics
     const int cw = atoi(wc) / FT_TEAM * FT_TEAM;
     if (cw >= FT_TEAM && cw < warps) warps = cw;
@@ -530,13 +590,8 @@ cudaError_t launch_fista_tile(const SolveParams& P, int num_sms, cudaStream_t st
   int maxq = (P.n + 31) / 32;
   maxq = maxq <= 1 ? 1 : maxq <= 2 ? 2 : 4;
   const int ct = (P.m + 127) / 128;
-  switch (ct) {
-    case 1: return launch_ft_q<1>(P, maxq, warps, smem, grid, st);
-    case 2: return launch_ft_q<2>(P, maxq, warps, smem, grid, st);
-    case 3: return launch_ft_q<3>(P, maxq, warps, smem, grid, st);
-    case 4: return launch_ft_q<4>(P, maxq, warps, smem, grid, st);
-    default: return cudaErrorInvalidValue;
-  }
+  if (team) return asmem ? launch_ft_ct<true, true>(P, ct, maxq, warps, smem, grid, st) : launch_ft_ct<false, true>(P, ct, maxq, warps, smem, grid, st);
+  return asmem ? launch_ft_ct<true, false>(P, ct, maxq, warps, smem, grid, st) : launch_ft_ct<false, false>(P, ct, maxq, warps, smem, grid, st);
 }
 
 }  // namespace tb

@@ -135,6 +135,10 @@ __global__ void __launch_bounds__(1024) tiled_schedule_kernel(const TiledParams 
 }
 
 // ------------------------------------------------------------------ fused pass
+#ifndef TB_TILED_FFMA2
+#define TB_TILED_FFMA2 0  // packed FFMA2 in the adjoint micro-tile: bit-identical, measured 6% SLOWER (cfg4/cfg5
+                          // FISTA: the pass is FMA-pipe bound, not issue bound), so scalar FFMA stays
+#endif
 constexpr int TL_AS = TL_CT + 1;  // odd row stride of the staged A tile
 constexpr int TL_ZS = TL_PT + 1;  // padded row stride of the staged candidate tile (conflict-free epilogue stores)
 
@@ -247,8 +251,8 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
         for (int i = 0; i < n; ++i) {
           const float4 r2 = *reinterpret_cast<const float4*>(&sRY[i * TL_PT + 2 * pp]);
           const float2 a = sA[i * TL_AS + c];
-          cfma_conj(g0, a, make_float2(r2.x, r2.y));
-          cfma_conj(g1, a, make_float2(r2.z, r2.w));
+          cfma_conj_x2(g0, a, conj_operand(r2.x, r2.y));
+          cfma_conj_x2(g1, a, conj_operand(r2.z, r2.w));
         }
         sG[(2 * pp) * TL_CT + c] = g0;
         sG[(2 * pp + 1) * TL_CT + c] = g1;
@@ -264,12 +268,19 @@ __global__ void __launch_bounds__(TL_THREADS, 2) tiled_pass_kernel(const TiledPa
     } else if (2 * pg < count)  // pixel pairs past the tile's count (few-RHS RBPG rounds) skip the GEMM
     for (int i = 0; i < n; ++i) {
       const float4 r2 = *reinterpret_cast<const float4*>(&sRY[i * TL_PT + 2 * pg]);
-      const float2 ra = make_float2(r2.x, r2.y), rbv = make_float2(r2.z, r2.w);
+      // packed FFMA2 (two per complex conj-MAC, the A element as the scalar-broadcast operand): the
+      // same per-component rounding sequence as cfma_conj, half the FMA instructions
+      const float4 ra = conj_operand(r2.x, r2.y), rbv = conj_operand(r2.z, r2.w);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float2 a = sA[i * TL_AS + cg + 16 * j];
-        cfma_conj(acc[0][j], a, ra);
-        cfma_conj(acc[1][j], a, rbv);
+#if TB_TILED_FFMA2
+        cfma_conj_x2(acc[0][j], a, ra);
+        cfma_conj_x2(acc[1][j], a, rbv);
+#else
+        cfma_conj(acc[0][j], a, make_float2(r2.x, r2.y));
+        cfma_conj(acc[1][j], a, make_float2(r2.z, r2.w));
+#endif
       }
     }
     // ---- epilogue: extrapolation + soft threshold in fp64 against the HBM state; all-zero state

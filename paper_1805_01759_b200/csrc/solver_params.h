@@ -67,9 +67,11 @@ __host__ __device__ inline size_t block_table_bytes(int J) {
 }
 
 cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps);
-// Team-tiled FISTA/ISTA kernel (k_fista_tile.cu): the dictionary must fit in shared memory beside
-// >= 8 pixel slots; m <= 512 (the extrapolation memory and the candidate live in tensor memory).
-bool fista_tile_fits(int n, int m);
-cudaError_t launch_fista_tile(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps);
+// ISTA/FISTA kernel with the extrapolation memory and the candidate in tensor memory
+// (k_fista_tile.cu): >= 8 pixel slots must fit in shared memory (beside the dictionary: *asmem; else
+// it is read from global memory); m <= 512.  *slots = resident pixel slots per SM.  team = the
+// 4-warp-team shared contraction (measured slower), else one warp per pixel.
+bool fista_tile_fits(int n, int m, bool* asmem, int* slots);
+cudaError_t launch_fista_tile(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps, bool team);
 
 }  // namespace tb

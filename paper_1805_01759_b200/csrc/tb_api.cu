@@ -825,10 +825,15 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   S.status = status;
   S.queue = c->queue;
   S.mk = c->mk;
-  // ISTA/FISTA with the dictionary in shared memory run the team-tiled kernel (TB_FISTA_KERNEL=warp
-  // selects the warp-per-pixel kernel: A/B and bit-identity tests)
+  // ISTA/FISTA: from one full wave of resident pixel slots the tensor-memory kernel (k_fista_tile.cu:
+  // 16 resident warps instead of 9 on cfg2, +24-32% on cfg2/cfg3); smaller batches are latency bound
+  // and run the unrolled warp kernel.  TB_FISTA_KERNEL=warp|solo|team overrides (A/B, identity tests).
   const char* fk = getenv("TB_FISTA_KERNEL");
-  const bool tile = solver != TB_SOLVER_RBPG && tb::fista_tile_fits((int)c->n, (int)c->m) && !(fk && strcmp(fk, "warp") == 0);
+  bool tile_asmem = false;
+  int tile_slots = 0;
+  const bool tile_fits = solver != TB_SOLVER_RBPG && tb::fista_tile_fits((int)c->n, (int)c->m, &tile_asmem, &tile_slots);
+  const bool team = fk && strcmp(fk, "team") == 0;
+  const bool tile = tile_fits && (fk ? (team || strcmp(fk, "solo") == 0) : P >= (int64_t)c->num_sms * tile_slots);
   if (solver == TB_SOLVER_RBPG && TB_WS_DCACHE) {
     const size_t need = (size_t)c->num_sms * 32 * (size_t)c->m;  // >= resident warp slots x m
     if (c->dglob_elems < need) {
@@ -846,7 +851,7 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
   int warps = 0;
   if (tile)
-    TB_CUDA(tb::launch_fista_tile(S, c->num_sms, st, &warps));
+    TB_CUDA(tb::launch_fista_tile(S, c->num_sms, st, &warps, team));
   else
     TB_CUDA(tb::launch_warp_solver(S, c->num_sms, st, &warps));
   TB_CUDA(ctx_release(c, st));

@@ -1,5 +1,5 @@
 OUT=gpurun_out/r3c; mkdir -p $OUT
-CFG=2 P=16384 BACKEND=fista PREC=fp64 timeout 900 ncu --set full --import-source on --clock-control none -k regex:fista_tile -c 1 -o $OUT/ft_full python tools/prof_one.py > $OUT/ncu_full.log 2>&1; echo "ncu rc=$?"
+TB_FISTA_KERNEL=${FK:-solo} CFG=${CFG:-2} P=${NP:-16384} BACKEND=fista PREC=fp64 timeout 900 ncu --set full --import-source on --clock-control none -k regex:fista_tile -c 1 -o $OUT/ft_full python tools/prof_one.py > $OUT/ncu_full.log 2>&1; echo "ncu rc=$?"
 ncu -i $OUT/ft_full.ncu-rep --page source --csv --print-source cuda,sass > $OUT/ft_source.csv 2>/dev/null
 ncu -i $OUT/ft_full.ncu-rep --page raw --csv > $OUT/ft_raw.csv 2>/dev/null
 ncu -i $OUT/ft_full.ncu-rep --page details > $OUT/ft_details.txt 2>/dev/null
