@@ -328,6 +328,7 @@ def run_b200(args):
         its_list.append(sol.iterations)  # summed after the timed region (no torch kernel inside it)
     ev1.record(stream)
     launches = tb._lib.launch_count() - launches0
+    solver_kernel = tb._lib.last_solver_kernel()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -401,7 +402,7 @@ def run_b200(args):
                 "step": "lambda + seeds + solve + select, whole batch",
             },
             "roofline": {
-                "bound": "fp32", "kernel": "warp_solver_kernel", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "bound": "fp32", "kernel": solver_kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu)", "traffic_source": traffic_src,
                 "peak_source": peak_src,
                 "algorithmic": f"{flop_pi:.0f} flop per pixel-iteration (16 n m{'/J' if args.backend == 'rbpg' else ''}) x {pix_iters / args.steps:.4g} pixel-iterations per launch",

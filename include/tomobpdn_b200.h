@@ -61,6 +61,10 @@ const char* tb_last_error(void);
 /* Number of kernels this library has launched since it was loaded (all entry points, all
    devices).  Instrumentation for the benchmark's gpu_launches claim; no reference counterpart. */
 int64_t tb_launch_count(void);
+/* Name of the solver kernel family the last tb_solve / tb_tiled_create of this process chose
+   ("warp_solver_kernel", "fista_tile_kernel<solo>", "fista_tile_kernel<team>", "tiled_pass_kernel").
+   Instrumentation for the benchmark's roofline line; no reference counterpart. */
+const char* tb_last_solver_kernel(void);
 
 /* Objective.dictionary (prox.py:25-63): copy a device complex64 [n, m] row-major matrix
  * (row = acquisition, column = flat grid index, model.py:317-323) into a new context. */

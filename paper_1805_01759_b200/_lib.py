@@ -40,6 +40,7 @@ SIGNATURES = {
     "tb_version": (ctypes.c_char_p, []),
     "tb_last_error": (ctypes.c_char_p, []),
     "tb_launch_count": (c_int64, []),
+    "tb_last_solver_kernel": (ctypes.c_char_p, []),
     "tb_ctx_create": (c_int32, [c_int32, c_void_p, c_int64, c_int64, ctypes.POINTER(c_void_p)]),
     "tb_ctx_destroy": (c_int32, [c_void_p]),
     "tb_spectral_sq_norms": (c_int32, [c_void_p, c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_void_p, c_int32, c_double, ctypes.POINTER(c_double), c_void_p]),
@@ -93,6 +94,11 @@ def check(code: int) -> None:
 def ptr(t) -> int:
     """Raw device pointer of a torch tensor (0 for None)."""
     return 0 if t is None else int(t.data_ptr())
+
+
+def last_solver_kernel() -> str:
+    """Kernel family the last solve chose (tb_last_solver_kernel)."""
+    return load().tb_last_solver_kernel().decode()
 
 
 def launch_count() -> int:

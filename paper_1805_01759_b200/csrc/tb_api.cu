@@ -139,6 +139,8 @@ static bool tiled_use_graph() {
 extern "C" {
 
 int64_t tb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+static std::atomic<const char*> g_last_kernel{"none"};
+const char* tb_last_solver_kernel(void) { return g_last_kernel.load(std::memory_order_relaxed); }
 const char* tb_version(void) { return "tomobpdn_b200 0.1.0 sm_100a"; }
 const char* tb_last_error(void) { return g_err.c_str(); }
 
@@ -391,6 +393,7 @@ int tb_tiled_create(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, cons
   int rc = check_solve_args(c, solver, cfg, seeds, P, hist, hist_stride);
   if (rc != TB_OK) return rc;
   if (!out || P < 1 || !pixels || !lam) return fail(TB_ERR_INVALID, "tiled solver needs >= 1 pixel and buffers");
+  g_last_kernel.store("tiled_pass_kernel", std::memory_order_relaxed);
   cudaStream_t st = (cudaStream_t)stream;
   TB_CUDA(cudaSetDevice(c->device));
   const int total = cfg->fixed_iters > 0 ? cfg->fixed_iters : cfg->max_iters;
@@ -850,6 +853,7 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   TB_CUDA(ctx_acquire(c, st));
   TB_CUDA(cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st));
   int warps = 0;
+  g_last_kernel.store(tile ? (team ? "fista_tile_kernel<team>" : "fista_tile_kernel<solo>") : "warp_solver_kernel", std::memory_order_relaxed);
   if (tile)
     TB_CUDA(tb::launch_fista_tile(S, c->num_sms, st, &warps, team));
   else
