@@ -43,7 +43,26 @@
 
 namespace tb {
 
-template <bool RB, int MAXT, int MAXQ, bool ASMEM, bool SHFL>
+// Tensor memory as a lane-private scratchpad (see k_fista_tile.cu): 4 consecutive 32-bit TMEM columns
+// = one double2 per lane, warp-uniform address, ~12-cycle LDTM, no shared-memory wavefront.
+__device__ __forceinline__ void ws_tmem_st(uint32_t taddr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(__double2loint(v.x)),
+               "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)), "r"(__double2hiint(v.y))
+               : "memory");
+}
+__device__ __forceinline__ double2 ws_tmem_ld(uint32_t taddr) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr) : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+}
+
+// XTM (RBPG whose dictionary does NOT fit in shared memory, cfg3): the fp64 iterate x and the per-block
+// delta cache live in tensor memory -- lane l keeps column cs_b + l + 32 t of block b at TMEM columns
+// 4 (b T + t), T = ceil(max width / 32), and row l + 32 q of delta_b at 4 (J T + b MAXQ + q).  A slot
+// shrinks by (m + J n) * 16 bytes (cfg3: 17.9 -> 3.3 KB), so 16 instead of 11 warps are resident AND
+// the unified L1/shared array keeps ~190 KB of L1 for the 200 KiB dictionary every iteration streams.
+template <bool RB, int MAXT, int MAXQ, bool ASMEM, bool SHFL, bool XTM>
 __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) warp_solver_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -86,20 +105,35 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
   // forward product, and delta_b is refreshed on accept from quantities already at hand:
   // A_b (z_b - x_b) = A_b dz + m_k delta_b.
   constexpr bool DC = RB && TB_WS_DCACHE;
-  const size_t per_warp = warp_slot_bytes_for(RB, n, m, P.max_width, J);
+  const size_t per_warp = warp_slot_bytes_for(RB, n, m, P.max_width, J) - (XTM ? ((size_t)m + (size_t)J * n) * 16 : 0);
   unsigned char* wb = smem + off + (size_t)warp * per_warp;
   double2* rv = reinterpret_cast<double2*>(wb);  // r (RBPG) / A x (FISTA)
   double2* apv = rv + n;                         // A x_prev (FISTA)
   double2* xs = DC ? rv + n : apv + n;           // x (fp64 iterate)
-  double2* zs = xs + m;                          // broadcast buffer for forward products [max_width]
+  double2* zs = xs + (XTM ? 0 : m);              // broadcast buffer for forward products [max_width]
   float4* ryv = reinterpret_cast<float4*>(zs + P.max_width);  // r_y rounded, as (r.x, r.y, r.y, -r.x)
   float2* ry2 = reinterpret_cast<float2*>(ryv);                // DC: r_y rounded, as (r.x, r.y)
   double2* ds = reinterpret_cast<double2*>(ryv + n);  // d = x - prev, fp64 (y = x + m_k d); not DC
   float2* bv = reinterpret_cast<float2*>(ds + m);  // b; not RBPG
   double2* dlt = reinterpret_cast<double2*>(ryv + n);  // DC: delta [J][n]
-  double* ring = DC ? reinterpret_cast<double*>(dlt + (size_t)J * n) : reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
+  double* ring = DC ? reinterpret_cast<double*>(dlt + (XTM ? 0 : (size_t)J * n)) : reinterpret_cast<double*>(bv + n);  // last STOP_WINDOW+1 objective values
   double* l1blk = ring + 16;                     // RBPG: sum |x_b| per block (updated on accept)
   double2* dg = DC ? P.dglob + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * m : nullptr;
+  // XTM: all 512 TMEM columns of this SM; warp w owns lanes 32 (w % 4) .. + 31 and 4 J T columns
+  __shared__ uint32_t tmem_base_s;
+  const int xt_t = (P.max_width + 31) >> 5;  // passes per block
+  uint32_t tm_x = 0;
+  if (XTM) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"((uint32_t)__cvta_generic_to_shared(&tmem_base_s)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    tm_x = tmem_base_s + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * (uint32_t)(4 * J * (xt_t + MAXQ));
+  }
+  const uint32_t tm_dl = tm_x + (uint32_t)(4 * J * xt_t);  // XTM: delta_b, lane = row i + 32 q at columns 4 (b MAXQ + q)
 
   // acc[q] += sum over the nonzero entries of the step (lane = row), fp64 accumulation.  L1 iterates
   // and their steps are sparse: the lanes compact the nonzero entries with __ballot_sync into
@@ -152,15 +186,19 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     const double lamd = (double)P.lam[p];
 
     // ---- initial state: x = 0, prev = 0, r = -b, F0 = ||b||^2 (solver.py:270-276, 349)
+    if (XTM) {
+      for (int e = 0; e < J * (xt_t + MAXQ); ++e) ws_tmem_st(tm_x + 4u * e, make_double2(0.0, 0.0));
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
     for (int c = lane; c < m; c += 32) {
-      xs[c] = make_double2(0.0, 0.0);
+      if (!XTM) xs[c] = make_double2(0.0, 0.0);
       if (DC)
         dg[c] = make_double2(0.0, 0.0);
       else
         ds[c] = make_double2(0.0, 0.0);
     }
     if (DC)
-      for (int e = lane; e < J * n; e += 32) dlt[e] = make_double2(0.0, 0.0);
+      for (int e = lane; e < (XTM ? 0 : J * n); e += 32) dlt[e] = make_double2(0.0, 0.0);
     double fb = 0.0;
     for (int i = lane; i < n; i += 32) {
       float2 b = P.B[(size_t)p * n + i];
@@ -270,7 +308,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         if (XR) xr[XR ? t : 0] = make_double2(0.0, 0.0);
         if (DC && (t == 0 || 32 * t < width)) {
           dvb[t] = dg[cs + min(lane + 32 * t, width - 1)];
-          if (XR) xr[XR ? t : 0] = xs[cs + min(lane + 32 * t, width - 1)];
+          if (XR) xr[XR ? t : 0] = XTM ? ws_tmem_ld(tm_x + 4u * (blk * xt_t + t)) : xs[cs + min(lane + 32 * t, width - 1)];
         }
       }
 #pragma unroll
@@ -316,8 +354,10 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         for (int q = 0; q < MAXQ; ++q) {
           const int i = lane + 32 * q;
           ry[q] = ay[q] = make_double2(0.0, 0.0);
+          double2 dlq = make_double2(0.0, 0.0);
+          if (XTM) dlq = ws_tmem_ld(tm_dl + 4u * (blk * MAXQ + q));
           if (i < n) {
-            const double2 r = rv[i], dl = dlt[blk * n + i];
+            const double2 r = rv[i], dl = XTM ? dlq : dlt[blk * n + i];
             ry[q] = make_double2(fma(mk, dl.x, r.x), fma(mk, dl.y, r.y));
             if (!SHFL) ry2[i] = make_float2((float)ry[q].x, (float)ry[q].y);
           }
@@ -395,7 +435,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
           const bool act = cl < width;
           const int col = cs + (act ? cl : 0);
           // y = x + m_k d; FISTA/ISTA recompute it from shared memory (keeps registers for occupancy)
-          const double2 xv = XR ? xr[XR ? t : 0] : xs[col];
+          // XTM: lanes past the block read their own (zero) cell; their results are masked
+          const double2 xv = XR ? xr[XR ? t : 0] : XTM ? ws_tmem_ld(tm_x + 4u * (blk * xt_t + t)) : xs[col];
           double2 yv = xv;
           if (DC) {
             yv.x = fma(mk, dvb[t].x, xv.x);
@@ -506,7 +547,13 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
         for (int t = 0; t < MAXT; ++t) {
           if (t > 0 && 32 * t >= width) continue;
           const int cl = lane + 32 * t;
-          if (cl < width) {
+          if (XTM) {
+            // warp-collective TMEM access: lanes past the block keep their zero
+            const double2 xv = XR ? xr[XR ? t : 0] : ws_tmem_ld(tm_x + 4u * (blk * xt_t + t));
+            const double2 zv = (accept && cl < width) ? z[RB ? t : 0] : xv;
+            if (accept) ws_tmem_st(tm_x + 4u * (blk * xt_t + t), zv);
+            if (cl < width) dg[cs + cl] = make_double2(zv.x - xv.x, zv.y - xv.y);
+          } else if (cl < width) {
             // accept: prev_b <- x_b, x_b <- z_b; reject: prev_b <- x_b (solver.py:318-325)
             const double2 xv = XR ? xr[XR ? t : 0] : xs[cs + cl], zv = accept ? z[RB ? t : 0] : xv;
             if (DC)
@@ -516,18 +563,23 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
             xs[cs + cl] = zv;
           }
         }
+        if (XTM && accept) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         if (DC) {
           // delta_b <- A_b (z_b - x_b) = A_b dz + A_b (y_b - x_b) = adz + m_k delta_b, or 0 on reject
 #pragma unroll
           for (int q = 0; q < MAXQ; ++q) {
             const int i = lane + 32 * q;
-            if (i < n) {
+            if (XTM) {
+              const double2 o = ws_tmem_ld(tm_dl + 4u * (blk * MAXQ + q));
+              ws_tmem_st(tm_dl + 4u * (blk * MAXQ + q), (accept && i < n) ? make_double2(fma(mk, o.x, adz[q].x), fma(mk, o.y, adz[q].y)) : make_double2(0.0, 0.0));
+            } else if (i < n) {
               double2* dl = dlt + blk * n + i;
               const double2 o = *dl;
               *dl = accept ? make_double2(fma(mk, o.x, adz[q].x), fma(mk, o.y, adz[q].y)) : make_double2(0.0, 0.0);
             }
           }
         }
+        if (XTM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         if (accept) {
 #pragma unroll
           for (int q = 0; q < MAXQ; ++q) {
@@ -587,6 +639,15 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       if (fabs(F - ref) <= P.tol * fmax(fabs(ref), 1e-300)) status = STATUS_CONVERGED;
     }
     __syncwarp();
+    if (XTM) {
+      for (int j = 0; j < J; ++j) {
+        const int c0 = s_bstart[j], w = s_bstart[j + 1] - c0;
+        for (int t = 0; 32 * t < w; ++t) {
+          const double2 xv = ws_tmem_ld(tm_x + 4u * (j * xt_t + t));
+          if (lane + 32 * t < w) P.X[(size_t)p * m + c0 + lane + 32 * t] = make_float2((float)xv.x, (float)xv.y);
+        }
+      }
+    } else
     for (int c = lane; c < m; c += 32) {
       const double2 xv = xs[c];
       P.X[(size_t)p * m + c] = make_float2((float)xv.x, (float)xv.y);
@@ -598,12 +659,20 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     }
     __syncwarp();
   }
+  if (XTM) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_s));
+  }
 }
 
 template <bool RB, int MAXT, int MAXQ, bool ASMEM>
-static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int grid, cudaStream_t st, bool shfl) {
+static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int grid, cudaStream_t st, bool shfl, bool xtm) {
   // r_y from shuffles only for RBPG (DC) batches smaller than the resident slots (see warp_adjoint.cuh)
-  auto k = (RB && TB_WS_DCACHE && shfl) ? warp_solver_kernel<RB, MAXT, MAXQ, ASMEM, true> : warp_solver_kernel<RB, MAXT, MAXQ, ASMEM, false>;
+  auto k = (RB && TB_WS_DCACHE && shfl) ? warp_solver_kernel<RB, MAXT, MAXQ, ASMEM, true, false> : warp_solver_kernel<RB, MAXT, MAXQ, ASMEM, false, false>;
+  if constexpr (RB && TB_WS_DCACHE && !ASMEM && MAXT <= 4) {
+    if (xtm) k = warp_solver_kernel<RB, MAXT, MAXQ, ASMEM, false, true>;
+  }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   count_launch();
@@ -612,22 +681,22 @@ static cudaError_t launch_t(const SolveParams& P, int warps, size_t smem, int gr
 }
 
 template <bool RB, int MAXT, bool ASMEM>
-static cudaError_t launch_q(const SolveParams& P, int maxq, int warps, size_t smem, int grid, cudaStream_t st, bool shfl) {
+static cudaError_t launch_q(const SolveParams& P, int maxq, int warps, size_t smem, int grid, cudaStream_t st, bool shfl, bool xtm) {
   switch (maxq) {
-    case 1: return launch_t<RB, MAXT, 1, ASMEM>(P, warps, smem, grid, st, shfl);
-    case 2: return launch_t<RB, MAXT, 2, ASMEM>(P, warps, smem, grid, st, shfl);
-    case 4: return launch_t<RB, MAXT, 4, ASMEM>(P, warps, smem, grid, st, shfl);
+    case 1: return launch_t<RB, MAXT, 1, ASMEM>(P, warps, smem, grid, st, shfl, xtm);
+    case 2: return launch_t<RB, MAXT, 2, ASMEM>(P, warps, smem, grid, st, shfl, xtm);
+    case 4: return launch_t<RB, MAXT, 4, ASMEM>(P, warps, smem, grid, st, shfl, xtm);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <bool RB, bool ASMEM>
-static cudaError_t launch_tq(const SolveParams& P, int maxt, int maxq, int warps, size_t smem, int grid, cudaStream_t st, bool shfl) {
-  if (maxt <= 2) return launch_q<RB, 2, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
-  if (maxt <= 4) return launch_q<RB, 4, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
-  if (maxt <= 8) return launch_q<RB, 8, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
-  if (maxt <= 12) return launch_q<RB, 12, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
-  if (maxt <= 16) return launch_q<RB, 16, ASMEM>(P, maxq, warps, smem, grid, st, shfl);
+static cudaError_t launch_tq(const SolveParams& P, int maxt, int maxq, int warps, size_t smem, int grid, cudaStream_t st, bool shfl, bool xtm) {
+  if (maxt <= 2) return launch_q<RB, 2, ASMEM>(P, maxq, warps, smem, grid, st, shfl, xtm);
+  if (maxt <= 4) return launch_q<RB, 4, ASMEM>(P, maxq, warps, smem, grid, st, shfl, xtm);
+  if (maxt <= 8) return launch_q<RB, 8, ASMEM>(P, maxq, warps, smem, grid, st, shfl, false);
+  if (maxt <= 12) return launch_q<RB, 12, ASMEM>(P, maxq, warps, smem, grid, st, shfl, false);
+  if (maxt <= 16) return launch_q<RB, 16, ASMEM>(P, maxq, warps, smem, grid, st, shfl, false);
   return cudaErrorInvalidValue;
 }
 
@@ -643,13 +712,27 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   const size_t tables = block_table_bytes(J);
   const bool cm = TB_WS_COLMAJOR && P.mode == SOLVER_RBPG;
   const size_t a_bytes = ((size_t)(cm ? (size_t)P.m * (P.n | 1) : (size_t)P.n * P.ms) * sizeof(float2) + 15) & ~(size_t)15;
-  const size_t cap = 227 * 1024;
+  const size_t cap = 227 * 1024 - 64;  // 16 static bytes (TMEM base address) + margin
   const int max_warps = maxt >= 8 ? TB_WARP_LB_WIDE / 32 : TB_WARP_LB / 32;
   bool asmem = a_bytes + tables + 4 * slot <= cap;
   size_t avail = cap - tables - (asmem ? a_bytes : 0);
-  int warps = (int)(avail / slot);
+  // RBPG whose dictionary is read through L1 (cfg3): x in tensor memory (TB_WS_XTM=0 disables)
+  bool xtm = false;
+  size_t slot_used = slot;
+  if (P.mode == SOLVER_RBPG && TB_WS_DCACHE && !asmem && maxt <= 4) {
+    const char* xe = getenv("TB_WS_XTM");
+    const int xcols = 4 * J * ((P.max_width + 31) / 32 + maxq);
+    const size_t slot_x = slot - ((size_t)P.m + (size_t)J * P.n) * 16;
+    int wx = (int)(avail / slot_x);
+    if (wx > max_warps) wx = max_warps;
+    if (!(xe && atoi(xe) == 0) && ((wx + 3) / 4) * xcols <= 512) {
+      xtm = true;
+      slot_used = slot_x;
+    }
+  }
+  int warps = (int)(avail / slot_used);
   if (warps > max_warps) warps = max_warps;
-  if (!asmem) {
+  if (!asmem && !xtm) {
     // dictionary read through L1/L2: RBPG leaves one slot's worth of the unified L1/shared array
     // to the L1 cache that serves A (cfg3: 11 instead of 12 warps is +5%; FISTA measured -2%, so
     // it keeps every slot; TB_WARPS_L1 overrides)
@@ -668,15 +751,15 @@ cudaError_t launch_warp_solver(const SolveParams& P, int num_sms, cudaStream_t s
   const bool spread = P.num_pixels < (long long)num_sms * warps;
   if (spread) warps = (int)((P.num_pixels + num_sms - 1) / num_sms);
   if (warps < 1) warps = 1;
-  size_t smem = (asmem ? a_bytes : 0) + tables + (size_t)warps * slot;
+  size_t smem = (asmem ? a_bytes : 0) + tables + (size_t)warps * slot_used;
   long long need = (P.num_pixels + warps - 1) / warps;
   int grid = num_sms;
   if (need < grid) grid = (int)need;
   if (grid < 1) grid = 1;
   if (used_warps) *used_warps = warps;
   const bool rb = P.mode == SOLVER_RBPG;
-  if (rb) return asmem ? launch_tq<true, true>(P, maxt, maxq, warps, smem, grid, st, spread) : launch_tq<true, false>(P, maxt, maxq, warps, smem, grid, st, spread);
-  return asmem ? launch_tq<false, true>(P, maxt, maxq, warps, smem, grid, st, false) : launch_tq<false, false>(P, maxt, maxq, warps, smem, grid, st, false);
+  if (rb) return asmem ? launch_tq<true, true>(P, maxt, maxq, warps, smem, grid, st, spread, false) : launch_tq<true, false>(P, maxt, maxq, warps, smem, grid, st, spread, xtm);
+  return asmem ? launch_tq<false, true>(P, maxt, maxq, warps, smem, grid, st, false, false) : launch_tq<false, false>(P, maxt, maxq, warps, smem, grid, st, false, false);
 }
 
 }  // namespace tb

@@ -382,7 +382,7 @@ static bool warp_path_fits(tb_ctx* c, int32_t solver) {
   if ((width + 31) / 32 > 16) return false;
   const int J = solver == TB_SOLVER_RBPG ? c->num_blocks : 1;
   const size_t slot = tb::warp_slot_bytes_for(solver == TB_SOLVER_RBPG, (int)c->n, (int)c->m, width, J);
-  return tb::block_table_bytes(J) + 4 * slot <= 227 * 1024;
+  return tb::block_table_bytes(J) + 4 * slot <= 227 * 1024 - 64;
 }
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }

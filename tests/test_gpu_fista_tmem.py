@@ -157,3 +157,42 @@ def test_edges_through_each_kernel(tb, kernel_env, name, backend):
     sol = tb.Dictionary(a).solve(b, np.array([0.2]), tb.SolverConfig(max_iters=300, tol=1e-6), backend)
     ref = O.SOLVERS[backend](a.astype(np.complex128), b[0].astype(np.complex128), 0.2, O.SolverCfg(max_iters=300, tol=1e-6), tb.Dictionary(a).lipschitz())
     assert int(sol.iterations[0]) == ref["iterations"] and int(sol.status[0]) == O.STATUS_CODES[ref["status"]]
+
+
+@pytest.mark.parametrize("npx", [1501, 40])
+def test_rbpg_tensor_memory_state_byte_identical(tb, npx):
+    """RBPG with the dictionary read through L1 (cfg3: 200 KiB): the kernel keeps x and the per-block
+    delta cache in tensor memory (TB_WS_XTM=0: in shared memory).  Same bytes either way, with every
+    warp count the launcher may pick."""
+    from paper_1805_01759_b200.synth import make_config
+
+    batch = make_config(3, num_pixels=npx)
+    d = tb.Dictionary(batch.dictionary)
+    px = torch.from_numpy(batch.pixels).cuda()
+    lam = d.default_lambda(px, 0.1)
+    seeds = d.derive_seeds(2018, npx)
+    old = {k: os.environ.get(k) for k in ("TB_WS_XTM", "TB_WARPS_CAP")}
+    try:
+        for kw in CONFIGS:
+            cfg = tb.SolverConfig(num_blocks=8, seed=2018, **kw)
+            res = {}
+            for name, env in (("smem", {"TB_WS_XTM": "0"}), ("tmem", {}), ("tmem5", {"TB_WARPS_CAP": "5"})):
+                for k in old:
+                    os.environ.pop(k, None)
+                os.environ.update(env)
+                res[name] = d.solve(px, lam, cfg, "rbpg", seeds=seeds, history=True)
+                torch.cuda.synchronize()
+            ref = res["smem"]
+            for name in ("tmem", "tmem5"):
+                got = res[name]
+                assert torch.equal(got.iterations, ref.iterations), (name, kw)
+                assert torch.equal(got.status, ref.status), (name, kw)
+                assert torch.equal(_bits(got.objective_final), _bits(ref.objective_final)), (name, kw)
+                assert torch.equal(_bits(got.x_hat), _bits(ref.x_hat)), (name, kw)
+                assert torch.equal(torch.nan_to_num(got.history, nan=-1.0), torch.nan_to_num(ref.history, nan=-1.0)), (name, kw)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
