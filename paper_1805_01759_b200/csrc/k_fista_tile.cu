@@ -17,6 +17,8 @@
 //   * the column passes of prox and update are rolled loops of 2-pass straight-line chunks (fully
 //     unrolled, 16 warps at different places of ~250 KB of code thrashed the instruction cache).
 // A slot is 10 KB on cfg2: 16 warps per SM, IPC 2.4, cfg2 FISTA 108 -> 82 ms per 65,536 pixels.
+// Variant GT (chosen when it makes more warps resident: cfg3, 12 -> 16): the gradient, which the same
+// lane produces and consumes, lives in tensor memory too, and instead of z only its shrink factor.
 //
 // TEAM = true is the 4-warp-team variant asked for by the round-1 review ("CTA-tiled dense
 // contraction"): a team iterates its 4 pixels in lock step and computes G = A^H R_y[:, 4 pixels]
@@ -43,8 +45,9 @@ constexpr int FT_CH = 64;    // compaction buffer entries (flushed every 2 colum
 
 // per-slot shared bytes: fp64 A x, A x_prev (n each), fp64 x (m), compaction values (FT_CH), r_y
 // quads (n), fp32 gradient (m), fp32 b (n), compaction columns (FT_CH), objective ring (16)
-__host__ __device__ inline size_t fista_tile_slot_bytes(int n, int m) {
-  size_t b = (size_t)n * 32 + (size_t)m * 16 + (size_t)FT_CH * 16 + (size_t)n * 16 + (size_t)m * 8 + (size_t)n * 8 + (size_t)FT_CH * 4 + 16 * 8;
+// (gsmem = false: the gradient lives in tensor memory, GT)
+__host__ __device__ inline size_t fista_tile_slot_bytes(int n, int m, bool gsmem) {
+  size_t b = (size_t)n * 32 + (size_t)m * 16 + (size_t)FT_CH * 16 + (size_t)n * 16 + (gsmem ? (size_t)m * 8 : 0) + (size_t)n * 8 + (size_t)FT_CH * 4 + 16 * 8;
   return (b + 15) & ~(size_t)15;
 }
 
@@ -75,6 +78,12 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, double2 v) {
 __device__ __forceinline__ void tmem_ld_issue(uint32_t taddr, uint32_t (&r)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr) : "memory");
 }
+__device__ __forceinline__ void tmem_st_x2(uint32_t taddr, uint32_t a, uint32_t b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void tmem_ld_issue_x2(uint32_t taddr, uint32_t (&r)[2]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr) : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ double2 tmem_val(const uint32_t (&r)[4]) { return make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2])); }
@@ -87,7 +96,9 @@ __device__ __forceinline__ double2 tmem_val(const uint32_t (&r)[4]) { return mak
 // with the column-lane adjoint of the warp kernel (warp_adjoint.cuh), keeping this kernel's compact
 // slot (d and z in tensor memory, 64-entry compaction buffer: 16 resident warps instead of the warp
 // kernel's 9 on cfg2).
-template <int CT, int MAXQ, bool ASMEM, bool TEAM>
+// GT (one warp per pixel only): the gradient and the candidate's shrink factor live in tensor memory
+// instead of g in shared memory and z in tensor memory; chosen when it makes more warps resident.
+template <int CT, int MAXQ, bool ASMEM, bool TEAM, bool GT>
 __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -106,11 +117,11 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
       reinterpret_cast<float2*>(smem)[(size_t)i * ms + c] = __ldg(&P.A[idx]);
     }
   int* s_act = reinterpret_cast<int*>(smem + a_bytes);  // [warps] slot-active flags
-  const size_t slot_bytes = fista_tile_slot_bytes(n, m);
+  const size_t slot_bytes = fista_tile_slot_bytes(n, m, !GT);
   unsigned char* slots = smem + a_bytes + 64 * sizeof(int);
   auto slot_ptr = [&](int s) { return slots + (size_t)s * slot_bytes; };
   const size_t off_xs = (size_t)n * 32, off_zs = off_xs + (size_t)m * 16, off_ry = off_zs + (size_t)FT_CH * 16;
-  const size_t off_g = off_ry + (size_t)n * 16, off_b = off_g + (size_t)m * 8, off_cl = off_b + (size_t)n * 8;
+  const size_t off_g = off_ry + (size_t)n * 16, off_b = off_g + (!GT ? (size_t)m * 8 : 0), off_cl = off_b + (size_t)n * 8;
   const size_t off_ring = (off_cl + (size_t)FT_CH * 4 + 7) & ~(size_t)7;
   unsigned char* wb = slot_ptr(warp);
   double2* axv = reinterpret_cast<double2*>(wb);       // A x
@@ -135,6 +146,13 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm_d = tmem_base_s + ((uint32_t)(wt * 32) << 16) + (uint32_t)team * 128u;
   const uint32_t tm_z = tm_d + 4u * (uint32_t)((m + 31) >> 5);
+  // GT: with one warp per pixel the gradient is produced and consumed by the same lane, so it can live
+  // in tensor memory too (fp32 pair, 2 columns per pass, at [6 T, 8 T)) if instead of the candidate z
+  // only its shrink factor sc = 1 - tau / |v| (0 where z = 0) is kept (fp64, [4 T, 6 T)): the update
+  // rebuilds z = (y - alpha g) sc from the same operands, bit for bit.  8 T columns as before, and the
+  // slot loses the m * 8 bytes of g (cfg3: 16.5 -> 12.5 KB, 16 instead of 12 resident warps: +8%; on
+  // cfg2, where 16 warps fit anyway, the rebuilt z costs 9%, so GT is used only when it adds warps).
+  const uint32_t tm_s = tm_z, tm_g = tm_z + 2u * (uint32_t)((m + 31) >> 5);
 
   const double alpha0_full = P.alpha_scale / fmax(P.lip_full, 1e-300);  // solver.py:345
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -240,9 +258,17 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
       const int passes = (m + 31) >> 5;
       adjoint_dispatch<1, MAXT, ASMEM, false>(passes, acc, As + lane, as, 32, ry4, n, lane + 32 * (passes - 1) < m);
 #pragma unroll
-      for (int t = 0; t < MAXT; ++t)
-        if (lane + 32 * t < m) gs[lane + 32 * t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
-      __syncwarp();
+      for (int t = 0; t < MAXT; ++t) {
+        if (GT) {
+          if (32 * t < m) tmem_st_x2(tm_g + 2u * t, __float_as_uint(2.f * acc[t].x), __float_as_uint(2.f * acc[t].y));
+        } else if (lane + 32 * t < m) {
+          gs[lane + 32 * t] = make_float2(2.f * acc[t].x, 2.f * acc[t].y);
+        }
+      }
+      if (GT)
+        tmem_wait_st();
+      else
+        __syncwarp();
     }
     if (TEAM) {
     if (lane == 0) s_act[warp] = active ? 1 : 0;
@@ -318,11 +344,11 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
     }
     // One column pass of the prox step for this lane's column lane + 32 t: z = soft(y - alpha g,
     // alpha lambda) with y = x + m_k d (d from tensor memory; its bits are garbage where dnz is clear)
-    auto prox_pass = [&](int t, double2 dv, double alpha, double tau, double tau2, double2& yv, double2& zz, double& absz) {
+    auto prox_pass = [&](int t, float2 g, double2 dv, double alpha, double tau, double tau2, double2& yv, double2& zz, double& absz, double& scz) {
       const int cl = lane + 32 * t;
       const bool act = cl < m;
       const int col = act ? cl : m - 1;
-      const float2 g = gs[col];
+      if (!GT) g = gs[col];
       double2 xv = make_double2(0.0, 0.0);
       if ((xnz >> t) & 1u) xv = xs[col];
       yv = xv;
@@ -334,12 +360,14 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
       const double mag2 = fma(v.x, v.x, v.y * v.y);
       zz = make_double2(0.0, 0.0);
       absz = 0.0;
+      scz = 0.0;
       // soft_threshold: zero iff |v| <= tau (prox.py:82-96); a NaN v stays NaN
       if (act && !(mag2 <= tau2)) {
         const double rs = rsqrt(mag2);
         const double sc = fma(-tau, rs, 1.0);
         zz = make_double2(v.x * sc, v.y * sc);
         absz = fma(mag2, rs, -tau);
+        scz = (zz.x != 0.0 || zz.y != 0.0) ? sc : 0.0;  // NaN z keeps its (NaN) factor
       }
     };
     double alpha = alpha0_full;
@@ -359,9 +387,13 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
 #pragma unroll 1
       for (int t0 = 0; 32 * t0 < m; t0 += 2) {
         const bool two = 32 * (t0 + 1) < m;
-        uint32_t dr[2][4];
+        uint32_t dr[2][4], gr[2][2] = {};
         tmem_ld_issue(tm_d + 4u * t0, dr[0]);
         tmem_ld_issue(tm_d + 4u * (two ? t0 + 1 : t0), dr[1]);
+        if (GT) {
+          tmem_ld_issue_x2(tm_g + 2u * t0, gr[0]);
+          tmem_ld_issue_x2(tm_g + 2u * (two ? t0 + 1 : t0), gr[1]);
+        }
         tmem_wait_ld();
         int cnt = 0;
 #pragma unroll
@@ -369,9 +401,12 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
           const int t = t0 + u;
           if (u == 1 && !two) break;
           double2 yv, zz;
-          double absz;
-          prox_pass(t, tmem_val(dr[u]), alpha, tau, tau2, yv, zz, absz);
-          tmem_st(tm_z + 4u * t, zz);
+          double absz, scz;
+          prox_pass(t, make_float2(__uint_as_float(gr[u][0]), __uint_as_float(gr[u][1])), tmem_val(dr[u]), alpha, tau, tau2, yv, zz, absz, scz);
+          if (!GT)
+            tmem_st(tm_z + 4u * t, zz);
+          else
+            tmem_st_x2(tm_s + 2u * t, (uint32_t)__double2loint(scz), (uint32_t)__double2hiint(scz));
           const bool act = lane + 32 * t < m;
           red[1] += absz;
           const double2 d = make_double2(zz.x - yv.x, zz.y - yv.y);
@@ -430,20 +465,43 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
 #pragma unroll 1
       for (int t0 = 0; 32 * t0 < m; t0 += 2) {
         const bool two = 32 * (t0 + 1) < m;
-        uint32_t zr[2][4];
-        tmem_ld_issue(tm_z + 4u * t0, zr[0]);
-        tmem_ld_issue(tm_z + 4u * (two ? t0 + 1 : t0), zr[1]);
+        uint32_t zr[2][4] = {}, dr[2][4] = {}, gr[2][2] = {}, sr[2][2] = {};
+        if (!GT) {
+          tmem_ld_issue(tm_z + 4u * t0, zr[0]);
+          tmem_ld_issue(tm_z + 4u * (two ? t0 + 1 : t0), zr[1]);
+        } else {
+          tmem_ld_issue(tm_d + 4u * t0, dr[0]);
+          tmem_ld_issue(tm_d + 4u * (two ? t0 + 1 : t0), dr[1]);
+          tmem_ld_issue_x2(tm_g + 2u * t0, gr[0]);
+          tmem_ld_issue_x2(tm_g + 2u * (two ? t0 + 1 : t0), gr[1]);
+          tmem_ld_issue_x2(tm_s + 2u * t0, sr[0]);
+          tmem_ld_issue_x2(tm_s + 2u * (two ? t0 + 1 : t0), sr[1]);
+        }
         tmem_wait_ld();
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int t = t0 + u;
           if (u == 1 && !two) break;
-          const double2 zz = tmem_val(zr[u]);  // 0 for lanes past m
           const int col = lane + 32 * t;
-          const bool zb = (zz.x != 0.0) || (zz.y != 0.0);
           const bool xb = (xnz >> t) & 1u;
           double2 xv = make_double2(0.0, 0.0);
           if (xb) xv = xs[col];
+          double2 zz;
+          if (!GT) {
+            zz = tmem_val(zr[u]);  // 0 for lanes past m
+          } else {
+            // z = (y - alpha g) sc from the operands of the accepted trial: the same roundings
+            const double scz = __hiloint2double((int)sr[u][1], (int)sr[u][0]);
+            double2 yv = xv;
+            if ((dnz >> t) & 1u) {
+              const double2 dv = tmem_val(dr[u]);
+              yv.x = fma(mk, dv.x, xv.x);
+              yv.y = fma(mk, dv.y, xv.y);
+            }
+            const double vx = fma(-alpha, (double)__uint_as_float(gr[u][0]), yv.x), vy = fma(-alpha, (double)__uint_as_float(gr[u][1]), yv.y);
+            zz = scz != 0.0 ? make_double2(vx * scz, vy * scz) : make_double2(0.0, 0.0);
+          }
+          const bool zb = (zz.x != 0.0) || (zz.y != 0.0);
           const double2 dn = make_double2(zz.x - xv.x, zz.y - xv.y);
           if (zb || xb) xs[col] = zz;  // implies col < m
           const bool nd = !ista && ((dn.x != 0.0) || (dn.y != 0.0));
@@ -513,30 +571,43 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
 }
 
 // Shared-memory plan: the dictionary beside >= 8 slots if it fits, else slots only (A from global)
-static bool fista_tile_plan(int n, int m, bool* asmem) {
+static bool fista_tile_plan(int n, int m, bool gsmem, bool* asmem) {
   if (m > 512 || n > 128) return false;  // 8 ceil(m / 32) tensor-memory columns per warp <= 128
-  const size_t cap = 227 * 1024 - 64, slot = fista_tile_slot_bytes(n, m);
+  const size_t cap = 227 * 1024 - 64, slot = fista_tile_slot_bytes(n, m, gsmem);
   const size_t a_bytes = (((size_t)n * (m | 1)) * sizeof(float2) + 15) & ~(size_t)15;
   const char* ev = getenv("TB_FISTA_TILE_ASMEM");  // 0: force the global-memory dictionary (A/B)
   const bool want = !(ev && atoi(ev) == 0);
   *asmem = want && a_bytes + 64 * sizeof(int) + 2 * FT_TEAM * slot <= cap;
   return *asmem || 64 * sizeof(int) + 2 * FT_TEAM * slot <= cap;
 }
-static int fista_tile_warps(int n, int m, bool asmem) {
-  const size_t slot = fista_tile_slot_bytes(n, m);
+static int fista_tile_warps(int n, int m, bool asmem, bool gsmem) {
+  const size_t slot = fista_tile_slot_bytes(n, m, gsmem);
   const size_t a_bytes = asmem ? (((size_t)n * (m | 1)) * sizeof(float2) + 15) & ~(size_t)15 : 0;
   const int warps = (int)((227 * 1024 - 64 - a_bytes - 64 * sizeof(int)) / slot);
   return warps > 16 ? 16 : warps / FT_TEAM * FT_TEAM;
 }
+// One-warp-per-pixel plan: g in shared memory unless g in tensor memory (GT) makes more warps resident
+static bool fista_solo_plan(int n, int m, bool* asmem, bool* gt, int* warps) {
+  bool as = false, ag = false;
+  const bool ok_s = fista_tile_plan(n, m, true, &as), ok_g = fista_tile_plan(n, m, false, &ag);
+  const int ws = ok_s ? fista_tile_warps(n, m, as, true) : 0, wg = ok_g ? fista_tile_warps(n, m, ag, false) : 0;
+  bool g = ok_g && (!ok_s || (ag == as && wg > ws));
+  if (const char* ge = getenv("TB_FISTA_GT")) g = ok_g && (atoi(ge) != 0 || !ok_s);  // A/B
+  *gt = g;
+  *asmem = g ? ag : as;
+  *warps = g ? wg : ws;
+  return ok_s || ok_g;
+}
 bool fista_tile_fits(int n, int m, bool* asmem, int* slots) {
-  bool a = false;
-  const bool ok = fista_tile_plan(n, m, &a);
+  bool a = false, g = false;
+  int w = 0;
+  const bool ok = fista_solo_plan(n, m, &a, &g, &w);
   if (asmem) *asmem = a;
-  if (slots) *slots = ok ? fista_tile_warps(n, m, a) : 0;
+  if (slots) *slots = ok ? w : 0;
   return ok;
 }
 
-template <int CT, bool ASMEM, bool TEAM>
+template <int CT, bool ASMEM, bool TEAM, bool GT>
 static cudaError_t launch_ft_q(const SolveParams& P, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -546,31 +617,36 @@ static cudaError_t launch_ft_q(const SolveParams& P, int maxq, int warps, size_t
     return cudaGetLastError();
   };
   switch (maxq) {
-    case 1: return go(fista_tile_kernel<CT, 1, ASMEM, TEAM>);
-    case 2: return go(fista_tile_kernel<CT, 2, ASMEM, TEAM>);
-    case 4: return go(fista_tile_kernel<CT, 4, ASMEM, TEAM>);
+    case 1: return go(fista_tile_kernel<CT, 1, ASMEM, TEAM, GT>);
+    case 2: return go(fista_tile_kernel<CT, 2, ASMEM, TEAM, GT>);
+    case 4: return go(fista_tile_kernel<CT, 4, ASMEM, TEAM, GT>);
     default: return cudaErrorInvalidValue;
   }
 }
-template <bool ASMEM, bool TEAM>
+template <bool ASMEM, bool TEAM, bool GT>
 static cudaError_t launch_ft_ct(const SolveParams& P, int ct, int maxq, int warps, size_t smem, int grid, cudaStream_t st) {
   switch (ct) {
-    case 1: return launch_ft_q<1, ASMEM, TEAM>(P, maxq, warps, smem, grid, st);
-    case 2: return launch_ft_q<2, ASMEM, TEAM>(P, maxq, warps, smem, grid, st);
-    case 3: return launch_ft_q<3, ASMEM, TEAM>(P, maxq, warps, smem, grid, st);
-    case 4: return launch_ft_q<4, ASMEM, TEAM>(P, maxq, warps, smem, grid, st);
+    case 1: return launch_ft_q<1, ASMEM, TEAM, GT>(P, maxq, warps, smem, grid, st);
+    case 2: return launch_ft_q<2, ASMEM, TEAM, GT>(P, maxq, warps, smem, grid, st);
+    case 3: return launch_ft_q<3, ASMEM, TEAM, GT>(P, maxq, warps, smem, grid, st);
+    case 4: return launch_ft_q<4, ASMEM, TEAM, GT>(P, maxq, warps, smem, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 // One CTA per SM, up to 16 pixel slots (4 teams); persistent, queue-fed.
 cudaError_t launch_fista_tile(const SolveParams& P, int num_sms, cudaStream_t st, int* used_warps, bool team) {
-  bool asmem = false;
-  if (!fista_tile_plan(P.n, P.m, &asmem)) return cudaErrorInvalidValue;
-  const size_t slot = fista_tile_slot_bytes(P.n, P.m);
+  bool asmem = false, gt = false;
+  int warps = 0;
+  if (team) {
+    if (!fista_tile_plan(P.n, P.m, true, &asmem)) return cudaErrorInvalidValue;
+    warps = fista_tile_warps(P.n, P.m, asmem, true);
+  } else if (!fista_solo_plan(P.n, P.m, &asmem, &gt, &warps)) {
+    return cudaErrorInvalidValue;
+  }
+  const size_t slot = fista_tile_slot_bytes(P.n, P.m, !gt);
   const size_t a_bytes = asmem ? (((size_t)P.n * P.ms) * sizeof(float2) + 15) & ~(size_t)15 : 0;
   const size_t fixed = a_bytes + 64 * sizeof(int);  // + 16 static bytes (TMEM base), inside the plan's margin
-  int warps = fista_tile_warps(P.n, P.m, asmem);
   if (const char* wc = getenv("TB_WARPS_CAP")) {  // tuning/diagnostics
     const int cw = atoi(wc) / FT_TEAM * FT_TEAM;
     if (cw >= FT_TEAM && cw < warps) warps = cw;
@@ -590,8 +666,9 @@ cudaError_t launch_fista_tile(const SolveParams& P, int num_sms, cudaStream_t st
   int maxq = (P.n + 31) / 32;
   maxq = maxq <= 1 ? 1 : maxq <= 2 ? 2 : 4;
   const int ct = (P.m + 127) / 128;
-  if (team) return asmem ? launch_ft_ct<true, true>(P, ct, maxq, warps, smem, grid, st) : launch_ft_ct<false, true>(P, ct, maxq, warps, smem, grid, st);
-  return asmem ? launch_ft_ct<true, false>(P, ct, maxq, warps, smem, grid, st) : launch_ft_ct<false, false>(P, ct, maxq, warps, smem, grid, st);
+  if (team) return asmem ? launch_ft_ct<true, true, false>(P, ct, maxq, warps, smem, grid, st) : launch_ft_ct<false, true, false>(P, ct, maxq, warps, smem, grid, st);
+  if (gt) return asmem ? launch_ft_ct<true, false, true>(P, ct, maxq, warps, smem, grid, st) : launch_ft_ct<false, false, true>(P, ct, maxq, warps, smem, grid, st);
+  return asmem ? launch_ft_ct<true, false, false>(P, ct, maxq, warps, smem, grid, st) : launch_ft_ct<false, false, false>(P, ct, maxq, warps, smem, grid, st);
 }
 
 }  // namespace tb

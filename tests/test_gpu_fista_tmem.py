@@ -21,7 +21,9 @@ pytestmark = pytest.mark.gpu
 
 from oracle import tomo_oracle as O  # noqa: E402
 
-KERNELS = ("warp", "solo", "team")
+# "solo+gt" / "solo-gt": force / forbid the variant that keeps the gradient (and the candidate's shrink
+# factor instead of the candidate) in tensor memory; by default it is chosen when it adds resident warps (cfg3)
+KERNELS = ("warp", "solo", "solo+gt", "solo-gt", "team")
 
 
 @pytest.fixture(scope="module")
@@ -35,16 +37,24 @@ def tb():
 
 @pytest.fixture
 def kernel_env():
-    old = os.environ.get("TB_FISTA_KERNEL")
+    old = {k: os.environ.get(k) for k in ("TB_FISTA_KERNEL", "TB_FISTA_GT")}
 
     def select(name):
-        if name is None:
-            os.environ.pop("TB_FISTA_KERNEL", None)
-        else:
-            os.environ["TB_FISTA_KERNEL"] = name
+        for k in old:
+            os.environ.pop(k, None)
+        if name is not None:
+            os.environ["TB_FISTA_KERNEL"] = name[:4]
+            if name.endswith("+gt"):
+                os.environ["TB_FISTA_GT"] = "1"
+            elif name.endswith("-gt"):
+                os.environ["TB_FISTA_GT"] = "0"
 
     yield select
-    select(old)
+    for k, v in old.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
 
 
 def _bits(t):
@@ -99,7 +109,7 @@ def test_default_choice_is_invisible(tb, kernel_env):
     assert torch.equal(_bits(big.objective_final[:64]), _bits(small.objective_final))
 
 
-@pytest.mark.parametrize("name", ["solo", "team"])
+@pytest.mark.parametrize("name", ["solo", "solo+gt", "team"])
 @pytest.mark.parametrize("backend", ["fista", "ista"])
 def test_golden_cfg1_through_each_kernel(tb, golden, kernel_env, name, backend):
     kernel_env(name)
@@ -117,7 +127,7 @@ def test_golden_cfg1_through_each_kernel(tb, golden, kernel_env, name, backend):
     np.testing.assert_allclose(bs.history.cpu().numpy()[:, :30], golden[f"cfg1/{backend}/hist"][:, :30], rtol=1e-5)
 
 
-@pytest.mark.parametrize("name", ["solo", "team"])
+@pytest.mark.parametrize("name", ["solo", "solo+gt", "team"])
 @pytest.mark.parametrize("backend", ["fista", "ista"])
 def test_edges_through_each_kernel(tb, kernel_env, name, backend):
     """NaN / inf measurements, lambda = 0, lambda above 2 max|A^H b|, a single pixel and a 33-column
