@@ -103,7 +103,9 @@ def test_default_choice_is_invisible(tb, kernel_env):
     lam = d.default_lambda(px, 0.1)
     cfg = tb.SolverConfig(max_iters=500, tol=1e-6)
     big = d.solve(px, lam, cfg, "fista")
+    assert tb._lib.last_solver_kernel() == "fista_tile_kernel<solo>"
     small = d.solve(px[:64], lam[:64], cfg, "fista")
+    assert tb._lib.last_solver_kernel() == "warp_solver_kernel"
     assert torch.equal(big.iterations[:64], small.iterations)
     assert torch.equal(_bits(big.x_hat[:64]), _bits(small.x_hat))
     assert torch.equal(_bits(big.objective_final[:64]), _bits(small.objective_final))
