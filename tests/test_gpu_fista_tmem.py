@@ -208,3 +208,32 @@ def test_rbpg_tensor_memory_state_byte_identical(tb, npx):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+
+
+@pytest.mark.parametrize("n,m,npx", [(10, 512, 2400), (33, 96, 2400), (64, 130, 300)])
+def test_kernels_byte_identical_other_shapes(tb, kernel_env, n, m, npx):
+    """Shapes off the BASELINE grid: 16 column passes with the dictionary in shared memory (all 512
+    tensor-memory columns in use, gradient in tensor memory by default), two row passes (n > 32) with
+    one and three column passes, batches above and below one wave of slots."""
+    rng = np.random.default_rng(n * 1000 + m)
+    a = (rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m))).astype(np.complex64) / np.sqrt(n)
+    b = (rng.standard_normal((npx, n)) + 1j * rng.standard_normal((npx, n))).astype(np.complex64)
+    d = tb.Dictionary(a)
+    px = torch.from_numpy(b).cuda()
+    lam = d.default_lambda(px, 0.1)
+    for backend in ("fista", "ista"):
+        for kw in (dict(max_iters=80, tol=1e-6), dict(max_iters=30, tol=1e-6, alpha_init_scale=4.0)):
+            cfg = tb.SolverConfig(**kw)
+            res = {}
+            for name in KERNELS:
+                kernel_env(name)
+                res[name] = d.solve(px, lam, cfg, backend, history=True)
+                torch.cuda.synchronize()
+            ref = res["warp"]
+            for name in KERNELS[1:]:
+                got = res[name]
+                assert torch.equal(got.iterations, ref.iterations), (name, backend, kw)
+                assert torch.equal(got.status, ref.status), (name, backend, kw)
+                assert torch.equal(_bits(got.objective_final), _bits(ref.objective_final)), (name, backend, kw)
+                assert torch.equal(_bits(got.x_hat), _bits(ref.x_hat)), (name, backend, kw)
+                assert torch.equal(torch.nan_to_num(got.history, nan=-1.0), torch.nan_to_num(ref.history, nan=-1.0)), (name, backend, kw)
