@@ -38,6 +38,27 @@ __global__ void __launch_bounds__(128) select_kernel(const SelectParams S) {
     const float2* x = S.X + (size_t)p * m;
     // ---- elevation profile + per-bin argmax over motion bins
     double peak = 0.0;
+    if (inner == 1) {
+      // elevation-only grids (cfg1-3): the lane's loads of x_hat are issued four at a time -- one
+      // dependent global load per loop trip left the warp waiting ~10 DRAM latencies per pixel
+      // (long scoreboard was the kernel's top stall); same values, same order of the max
+      for (int s0 = lane; s0 < ne; s0 += 128) {
+        float2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = s0 + 32 * u < ne ? x[s0 + 32 * u] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int s = s0 + 32 * u;
+          if (s < ne) {
+            const double a = sqrt((double)v[u].x * v[u].x + (double)v[u].y * v[u].y);
+            const double best = a > -1.0 ? a : -1.0;  // a NaN magnitude reads as -1, as below
+            prof[s] = best;
+            amx[s] = 0;
+            peak = fmax(peak, best);
+          }
+        }
+      }
+    } else
     for (int s = lane; s < ne; s += 32) {
       double best = -1.0;
       int arg = 0;
