@@ -161,14 +161,14 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
   auto forward_accum = [&](int cnt, double2* acc) {
     const float2* arow[MAXQ];
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) arow[q] = As + (size_t)min(lane + 32 * q, n - 1) * as;
+    for (int q = 0; q < MAXQ; ++q) arow[q] = ASMEM ? As + (size_t)min(lane + 32 * q, n - 1) * as : P.AT + min(lane + 32 * q, n - 1);  // global: column-major copy
     int e = 0;
     for (; e + 2 <= cnt; e += 2) {
       const int2 cc = *reinterpret_cast<const int2*>(clist + e);
       const double2 v0 = zs[e], v1 = zs[e + 1];
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const float2 a0 = ASMEM ? arow[q][cc.x] : __ldg(arow[q] + cc.x), a1 = ASMEM ? arow[q][cc.y] : __ldg(arow[q] + cc.y);
+        const float2 a0 = ASMEM ? arow[q][cc.x] : __ldg(arow[q] + (size_t)cc.x * n), a1 = ASMEM ? arow[q][cc.y] : __ldg(arow[q] + (size_t)cc.y * n);
         acc[q].x = fma((double)a0.x, v0.x, fma(-(double)a0.y, v0.y, acc[q].x));
         acc[q].y = fma((double)a0.x, v0.y, fma((double)a0.y, v0.x, acc[q].y));
         acc[q].x = fma((double)a1.x, v1.x, fma(-(double)a1.y, v1.y, acc[q].x));
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(512, 1) fista_tile_kernel(const SolveParams P)
       const double2 v = zs[e];
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const float2 a = ASMEM ? arow[q][c] : __ldg(arow[q] + c);
+        const float2 a = ASMEM ? arow[q][c] : __ldg(arow[q] + (size_t)c * n);
         acc[q].x = fma((double)a.x, v.x, fma(-(double)a.y, v.y, acc[q].x));
         acc[q].y = fma((double)a.x, v.y, fma((double)a.y, v.x, acc[q].y));
       }

@@ -556,4 +556,24 @@ cudaError_t launch_apply_filter(const double2* W, int n, int m, const float2* B,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- column-major copy of the dictionary
+__global__ void transpose_kernel(const float2* __restrict__ A, int n, int m, float2* __restrict__ AT) {
+  __shared__ float2 tile[32][33];
+  const int c0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + r, c = c0 + threadIdx.x;
+    if (i < n && c < m) tile[r][threadIdx.x] = A[(size_t)i * m + c];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int c = c0 + r, i = i0 + threadIdx.x;
+    if (i < n && c < m) AT[(size_t)c * n + i] = tile[threadIdx.x][r];
+  }
+}
+cudaError_t launch_transpose(const float2* A, int n, int m, float2* AT, cudaStream_t st) {
+  count_launch();
+  transpose_kernel<<<dim3((m + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, st>>>(A, n, m, AT);
+  return cudaGetLastError();
+}
+
 }  // namespace tb

@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
     for (int q = 0; q < MAXQ; ++q) {
       acc[q] = make_double2(0.0, 0.0);
       const int i = min(lane + 32 * q, n - 1);
-      arow[q] = CM ? As + i : ASMEM ? As + i * ms : P.A + (size_t)i * m;  // CM: cl holds column * ns
+      // CM: cl holds column * ns; A not in shared memory: the column-major copy, element (i, c) at c n + i
+      arow[q] = CM ? As + i : ASMEM ? As + i * ms : P.AT + i;
     }
     int e = 0;
     for (; e + 2 <= cnt; e += 2) {
@@ -153,8 +154,8 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       const double2 v0 = zs[e], v1 = zs[e + 1];
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const float2 a0 = ASMEM ? arow[q][cc.x] : __ldg(arow[q] + cc.x);
-        const float2 a1 = ASMEM ? arow[q][cc.y] : __ldg(arow[q] + cc.y);
+        const float2 a0 = ASMEM ? arow[q][cc.x] : __ldg(arow[q] + (size_t)cc.x * n);
+        const float2 a1 = ASMEM ? arow[q][cc.y] : __ldg(arow[q] + (size_t)cc.y * n);
         acc[q].x = fma((double)a0.x, v0.x, fma(-(double)a0.y, v0.y, acc[q].x));
         acc[q].y = fma((double)a0.x, v0.y, fma((double)a0.y, v0.x, acc[q].y));
         acc[q].x = fma((double)a1.x, v1.x, fma(-(double)a1.y, v1.y, acc[q].x));
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(MAXT >= 8 ? TB_WARP_LB_WIDE : TB_WARP_LB, 1) w
       const double2 v = zs[e];
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const float2 a = ASMEM ? arow[q][c] : __ldg(arow[q] + c);
+        const float2 a = ASMEM ? arow[q][c] : __ldg(arow[q] + (size_t)c * n);
         acc[q].x = fma((double)a.x, v.x, fma(-(double)a.y, v.y, acc[q].x));
         acc[q].y = fma((double)a.x, v.y, fma((double)a.y, v.x, acc[q].y));
       }

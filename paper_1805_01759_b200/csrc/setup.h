@@ -9,6 +9,8 @@ namespace tb {
 
 cudaError_t launch_default_lambda(const float2* A, int n, int m, const float2* B, long long P, double beta,
                                   double* lam, int num_sms, cudaStream_t st);
+// AT[c][i] = A[i][c] (complex64)
+cudaError_t launch_transpose(const float2* A, int n, int m, float2* AT, cudaStream_t st);
 cudaError_t launch_derive_seeds(uint64_t run_seed, long long first, long long P, uint64_t* seeds, cudaStream_t st);
 cudaError_t launch_synth_pair(const float2* A, int n, int m, uint64_t seed, const uint64_t* stream_ids, const int* c0,
                               const int* c1, const float* phase, const float* sigma, long long count, float2* pixels,

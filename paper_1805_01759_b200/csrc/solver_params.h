@@ -13,6 +13,7 @@ constexpr int STOP_WINDOW = 10;  // solver.py:29
 
 struct SolveParams {
   const float2* A;  // device [n][m] row-major complex64
+  const float2* AT; // device [m][n] (column-major copy of A), read by the forward products when A is not in shared memory
   int n, m, ms;     // ms: odd shared-memory row stride (>= m)
   int mode;
   int num_blocks;

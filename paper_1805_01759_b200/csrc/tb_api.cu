@@ -19,6 +19,7 @@ struct tb_ctx {
   int num_sms = 148;
   int64_t n = 0, m = 0;
   float2* A = nullptr;  // owned copy, [n][m]
+  float2* AT = nullptr; // [m][n] transpose, built on first use by the kernels that read A through L1
   // partition
   int num_blocks = 0;
   int* blk_start = nullptr;  // device [J+1]
@@ -174,6 +175,7 @@ int tb_ctx_destroy(tb_ctx* c) {
   ctx_drain(c);
   if (c->done) cudaEventDestroy(c->done);
   cudaFree(c->A);
+  cudaFree(c->AT);
   cudaFree(c->blk_start);
   cudaFree(c->blk_lip);
   cudaFree(c->cdf);
@@ -799,7 +801,15 @@ int tb_solve(tb_ctx* c, int32_t solver, const tb_solver_config* cfg, const void*
   if (!warp_path_fits(c, solver))
     return solve_tiled(c, solver, cfg, pixels, lam, seeds, P, x, f_final, hist, hist_stride, iters, status, st);
   tb::SolveParams S{};
+  if (!c->AT) {
+    // column-major copy for the kernels that read the dictionary through L1 (cfg3): their sparse
+    // forward product reads whole columns, contiguous here, one 128-byte line per 16 rows instead
+    // of one line per row
+    TB_CUDA(cudaMalloc((void**)&c->AT, sizeof(float2) * c->n * c->m));
+    TB_CUDA(tb::launch_transpose(c->A, (int)c->n, (int)c->m, c->AT, st));
+  }
   S.A = c->A;
+  S.AT = c->AT;
   S.n = (int)c->n;
   S.m = (int)c->m;
   S.ms = (int)(c->m | 1);
